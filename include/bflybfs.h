@@ -1,0 +1,145 @@
+/*
+ * bflybfs.h -- C ABI of libbflybfs.so, the B200 (sm_100a) ButterFly BFS path.
+ *
+ * This library fills the native-kernel slot the reference declares but does
+ * not ship (`bflybfs._kernels._ext`, pkg/setup.py:5-15; "compiled kernels are
+ * built for uint32", pkg/src/bflybfs/graphs.py:11-12).  Every entry point
+ * below names the reference interface it replaces.  Plain pointers and sizes
+ * only; host arrays are borrowed for the duration of a call; the context owns
+ * all device memory.  Return value 0 = success, negative = error (see codes);
+ * bfb_last_error() gives the message of the last failure on this thread.
+ *
+ * Vertex ids are uint32 (graphs.py:13 VID), distances use UNREACHED =
+ * 0xFFFFFFFF (graphs.py:17), offsets are int64 (graphs.py:59).
+ */
+#ifndef BFLYBFS_H_
+#define BFLYBFS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes: the Python wrapper maps them to the reference's exceptions */
+#define BFB_OK 0
+#define BFB_ERR_INVALID (-1)        /* ValueError: bad argument                        */
+#define BFB_ERR_ROOT (-2)           /* ValueError: root out of range */
+#define BFB_ERR_PARTITION (-3)      /* ValueError: partition/graph mismatch */
+#define BFB_ERR_FANOUT (-4)         /* ValueError: fanout > CN           */
+#define BFB_ERR_SELF_EDGE (-5)      /* ValueError: graphs.py:240                       */
+#define BFB_ERR_DUPLICATE (-6)      /* ValueError: graphs.py:244                       */
+#define BFB_ERR_NO_REVERSE (-7)     /* ValueError: graphs.py:247                       */
+#define BFB_ERR_RANGE (-8)          /* ValueError: endpoint >= num_vertices (graphs.py:44-45) */
+#define BFB_ERR_STATE (-9)          /* RuntimeError: call order (no graph / no engine) */
+#define BFB_ERR_CAPACITY (-10)      /* RuntimeError: buffer-bound violation */
+#define BFB_ERR_CUDA (-20)          /* RuntimeError: CUDA failure                      */
+#define BFB_ERR_OOM (-21)           /* MemoryError: device allocation failed           */
+
+#define BFB_STRATEGY_BUTTERFLY 0    /* SPEC.md:280 strategy = butterfly                */
+#define BFB_STRATEGY_ALL2ALL 1      /* SPEC.md:280 strategy = all-to-all */
+
+typedef struct bfb_ctx bfb_ctx;
+
+/* RunStats plus device-side phase timings. */
+typedef struct bfb_run_stats {
+  int64_t levels;                    /* non-empty frontiers, = 1 + eccentricity       */
+  int64_t rounds_executed;           /* butterfly rounds summed over levels           */
+  int64_t remote_messages;           /* non-empty scheduled transfers   */
+  int64_t remote_vertices;           /* sum of transferred snapshot sizes             */
+  int64_t traversed_edges;           /* sum of deg(v) over reached v    */
+  int64_t reached;                   /* vertices with a finite distance               */
+  int64_t buffer_high_water_max;     /* max over nodes of per-round incoming vertices */
+  int64_t exchange_bytes;            /* bytes the exchange moved between nodes        */
+  double elapsed_ms;                 /* device time, root injection -> termination    */
+  double expand_ms;                  /* phase 1 kernels (timing mode only)            */
+  double exchange_ms;                /* phase 2 kernels (timing mode only)            */
+  double commit_ms;                  /* level commit / frontier build (timing mode)   */
+  int64_t expand_launches;           /* expand kernel launches in this run            */
+  int64_t kernel_launches;           /* all kernels this library launched in the run  */
+} bfb_run_stats;
+
+/* ---- library ---------------------------------------------------------- */
+const char* bfb_version(void);
+const char* bfb_last_error(void);
+int bfb_device_count(int* count_out);
+
+/* ---- butterfly-schedule (host-only, no GPU needed) ------ */
+/* num_rounds(CN, f): SPEC.md:202-210 */
+int bfb_num_rounds(int num_nodes, int fanout, int* rounds_out);
+/* make_schedule(CN, f) or the all2all pattern.
+ * Flattened into `out`: for each round, for each node g: count c, then c source ids.
+ * *len_out = int32 entries written (or needed, if cap is too small -> BFB_ERR_INVALID). */
+int bfb_make_schedule(int num_nodes, int fanout, int strategy, int32_t* out, int64_t cap,
+                      int64_t* len_out);
+/* message_count_paper */
+int bfb_message_count_paper(int num_nodes, int fanout, int64_t* out);
+/* buffer_bound */
+int64_t bfb_buffer_bound(int64_t num_vertices, int fanout);
+
+/* ---- context ----------------------------------------------------------- */
+int bfb_create(bfb_ctx** ctx_out, int device);
+void bfb_destroy(bfb_ctx* ctx);
+/* Record per-phase CUDA events inside bfb_bfs (fills *_ms of bfb_run_stats). */
+int bfb_set_timing(bfb_ctx* ctx, int enabled);
+
+/* ---- graph-core on device (graphs.py) ------------------------------------ */
+/* generate_rmat (graphs.py:254-285): raw edges to a HOST buffer of 2*m uint32
+ * (m = edge_factor << scale).  pcg_state/pcg_inc = numpy PCG64 initial state of
+ * default_rng(seed) as {hi, lo}; thresholds = ceil(p * 2^53) for
+ * (p_bottom, p_right_top, p_right_bottom) of graphs.py:273-275. */
+int bfb_rmat_edges(bfb_ctx* ctx, int scale, int64_t edge_factor, const uint64_t pcg_state[2],
+                   const uint64_t pcg_inc[2], const uint64_t thresholds[3], uint32_t* edges_out);
+/* generate_rmat -> symmetrize -> build_csr fused on device; the CSR stays
+ * resident in ctx (replaces graphs.py:218-251 for synthetic inputs). */
+int bfb_graph_from_rmat(bfb_ctx* ctx, int scale, int64_t edge_factor,
+                        const uint64_t pcg_state[2], const uint64_t pcg_inc[2],
+                        const uint64_t thresholds[3]);
+/* symmetrize (graphs.py:218-230) when `symmetrize` != 0, else build_csr's
+ * validation (graphs.py:238-247) of an already symmetrized list.  Edges are
+ * 2*m uint32 host values (src, dst) pairs; the CSR stays resident in ctx. */
+int bfb_graph_from_edges(bfb_ctx* ctx, int64_t num_vertices, const uint32_t* edges, int64_t m,
+                         int symmetrize);
+/* Upload an existing CSR (reference Graph, graphs.py:53-64). */
+int bfb_graph_load_csr(bfb_ctx* ctx, int64_t num_vertices, int64_t num_edges,
+                       const int64_t* offsets, const uint32_t* adjacency);
+int bfb_graph_info(bfb_ctx* ctx, int64_t* num_vertices_out, int64_t* num_edges_out,
+                   int64_t* max_degree_out);
+/* D2H of the resident CSR (offsets n+1 int64, adjacency m uint32); either may be NULL. */
+int bfb_graph_copy_csr(bfb_ctx* ctx, int64_t* offsets_out, uint32_t* adjacency_out);
+/* D2H of the resident graph as the sorted, deduplicated (src, dst) list (2*m uint32). */
+int bfb_graph_copy_edges(bfb_ctx* ctx, uint32_t* edges_out);
+/* partition_1d (graphs.py:288-305) on the resident CSR: num_parts+1 int64. */
+int bfb_partition_1d(bfb_ctx* ctx, int num_parts, int64_t* boundaries_out);
+/* Number of vertices with degree > 0, and the vertices at the given ranks among
+ * them (ascending id order): device form of flatnonzero(degrees > 0)[ranks]. */
+int bfb_count_nonisolated(bfb_ctx* ctx, int64_t* count_out);
+int bfb_select_nonisolated(bfb_ctx* ctx, const int64_t* ranks, int64_t k, int64_t* vertices_out);
+
+/* ---- engine ------------------------------------------- */
+/* init's allocation step: CN = num_parts nodes over the
+ * resident graph with the given partition (num_parts+1 boundaries), all
+ * per-node buffers allocated once here (no allocation inside bfb_bfs). */
+int bfb_engine_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int fanout,
+                     int strategy, int want_parents);
+/* run: one BFS from root.  levels_out (n uint32) and
+ * parents_out (n int64, -1 unreached, root->root) are host buffers and may be
+ * NULL (results stay on device).  frontier_sizes_out holds up to max_levels
+ * entries (per_level_frontier_size); buffer_high_water_out holds num_parts
+ * entries (may be NULL). */
+int bfb_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_out,
+            int64_t* frontier_sizes_out, int64_t max_levels, int64_t* buffer_high_water_out,
+            bfb_run_stats* stats_out);
+/* D2H of the last run's results (node 0's view). */
+int bfb_copy_levels(bfb_ctx* ctx, uint32_t* levels_out);
+int bfb_copy_parents(bfb_ctx* ctx, int64_t* parents_out);
+/* Device-side certificate of the last run's levels and
+ * parents: *errors_out = bitmask (1 root, 2 reachability mismatch on an edge,
+ * 4 edge spans >1 level, 8 reached vertex without predecessor, 16 bad parent). */
+int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFLYBFS_H_ */

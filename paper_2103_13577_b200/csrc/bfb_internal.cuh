@@ -1,0 +1,248 @@
+// Internal declarations shared by the libbflybfs translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bflybfs.h"
+
+namespace bfb {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define BFB_CUDA(call)                                                  \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) return ::bfb::cuda_fail(e_, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define BFB_TRY(call)             \
+  do {                            \
+    int rc_ = (call);             \
+    if (rc_ != BFB_OK) return rc_; \
+  } while (0)
+
+// ------------------------------------------------------- device buffers --
+// Owning device allocation.  All engine buffers are created in setup calls;
+// bfb_bfs itself never allocates.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  int alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return fail(BFB_ERR_OOM, "device allocation of " + std::to_string(count * sizeof(T)) +
+                                   " bytes failed: " + cudaGetErrorString(e));
+    }
+    n = count;
+    return BFB_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// ------------------------------------------------------------- PCG64 -----
+// numpy's PCG64: 128-bit LCG, state stepped before output, XSL-RR output,
+// random() = (next64 >> 11) * 2^-53.  An affine map x -> a*x + c (mod 2^128)
+// represents "advance by k steps", so jump-ahead is square-and-multiply.
+struct U128 {
+  uint64_t hi, lo;
+};
+
+__host__ __device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+__host__ __device__ __forceinline__ U128 mul128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = mulhi64(a.lo, b.lo) + a.hi * b.lo + a.lo * b.hi;
+  return r;
+}
+
+__host__ __device__ __forceinline__ U128 add128(U128 a, U128 b) {
+  U128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1 : 0);
+  return r;
+}
+
+struct Affine {
+  U128 a, c;  // x -> a*x + c
+};
+
+__host__ __device__ __forceinline__ U128 apply(const Affine& f, U128 x) {
+  return add128(mul128(f.a, x), f.c);
+}
+
+// g after f
+__host__ __device__ __forceinline__ Affine compose(const Affine& g, const Affine& f) {
+  Affine r;
+  r.a = mul128(g.a, f.a);
+  r.c = add128(mul128(g.a, f.c), g.c);
+  return r;
+}
+
+__host__ __device__ __forceinline__ Affine affine_pow(Affine step, uint64_t k) {
+  Affine acc;
+  acc.a = U128{0, 1};
+  acc.c = U128{0, 0};
+  while (k) {
+    if (k & 1) acc = compose(step, acc);
+    step = compose(step, step);
+    k >>= 1;
+  }
+  return acc;
+}
+
+__host__ __device__ __forceinline__ uint64_t xsl_rr(U128 s) {
+  uint64_t x = s.hi ^ s.lo;
+  unsigned rot = (unsigned)(s.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+constexpr uint64_t kPcgMultHi = 0x2360ED051FC65DA4ULL;
+constexpr uint64_t kPcgMultLo = 0x4385DF649FCCF645ULL;
+
+// ------------------------------------------------------------ graph -------
+struct DevGraph {
+  int64_t n = 0, m = 0, max_degree = 0;
+  DevBuf<int64_t> offsets;   // n+1
+  DevBuf<uint32_t> adj;      // m
+  bool valid = false;
+};
+
+// ------------------------------------------------------------ engine ------
+// Device-resident counters of one node (compute node = part).
+struct PartCounters {
+  int64_t q_count;      // |q_local| (owned frontier)
+  int64_t q_edges;      // sum of degrees over q_local
+  int64_t frontier;     // |synchronized next frontier| counted at commit
+  int64_t pub_count[2]; // published snapshot size, by round parity (phase 2)
+  uint32_t ticket;      // dynamic block ids for the look-back scan
+  uint32_t pad;
+};
+
+// Device-resident run statistics (RunStats).
+struct RunCounters {
+  int64_t remote_messages;
+  int64_t remote_vertices;
+  int64_t traversed_edges;
+  int64_t reached;
+  int64_t exchange_bytes;
+};
+
+// One compute node's private world (NodeState).
+struct Part {
+  int64_t lo = 0, hi = 0;          // owned vertex range [lo, hi)
+  int64_t wlo = 0, whi = 0;        // words touching the owned range
+  int64_t owned_edges = 0;
+  int64_t tile_cap = 0;
+  DevBuf<uint32_t> visited;        // replicated visited bitmap (n bits)
+  DevBuf<uint32_t> start;          // visited as of the level start
+  DevBuf<uint32_t> level;          // d_local (n)
+  DevBuf<uint32_t> parent;         // phase-1 parents (n) when wanted
+  DevBuf<uint32_t> pub;            // published round snapshot (n bits)
+  DevBuf<uint32_t> q_v;            // q_local vertex ids, ascending
+  DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local
+  DevBuf<int64_t> q_row;           // offsets[v] of each q_local vertex
+  DevBuf<uint32_t> tile_vstart;    // q_local index owning edge t*TILE
+  DevBuf<uint64_t> scan_state;     // look-back tile status (2 words / tile)
+  DevBuf<PartCounters> ctr;
+};
+
+}  // namespace bfb
+
+namespace bfb {
+struct EngineTables;  // bfs_engine.cu: device-side pointer/schedule tables
+}
+
+struct bfb_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  bfb::DevGraph g;
+  // engine
+  bool engine_ready = false;
+  int num_parts = 0, fanout = 1, strategy = 0, want_parents = 0;
+  std::vector<int64_t> bounds;
+  std::vector<std::vector<std::vector<int>>> schedule;  // [round][node] -> sources
+  std::vector<bfb::Part> parts;
+  bfb::DevBuf<bfb::RunCounters> run;
+  bfb::DevBuf<int64_t> high_water;    // per node
+  int64_t* pinned = nullptr;          // host scratch (pinned)
+  bfb::EngineTables* tables = nullptr;
+  int expand_grid = 0;
+  bool timing = false;
+  bool have_run = false;
+  int64_t last_root = -1;
+  int64_t last_levels = 0;
+  int64_t launches = 0;
+};
+
+namespace bfb {
+
+// graph_build.cu
+int build_from_rmat(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc,
+                    const uint64_t thr[3]);
+int build_from_edges(bfb_ctx* ctx, int64_t n, const uint32_t* host_edges, int64_t m,
+                     bool symmetrize);
+int rmat_to_host(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc, const uint64_t thr[3],
+                 uint32_t* out);
+int load_csr(bfb_ctx* ctx, int64_t n, int64_t m, const int64_t* offsets, const uint32_t* adj);
+int copy_edges(bfb_ctx* ctx, uint32_t* out);
+int partition_1d(bfb_ctx* ctx, int parts, int64_t* out);
+int count_nonisolated(bfb_ctx* ctx, int64_t* out);
+int select_nonisolated(bfb_ctx* ctx, const int64_t* ranks, int64_t k, int64_t* out);
+
+// scan.cu: exclusive scan of n values produced by a loader -> int64 out[0..n]
+// (out[n] = total).  Work buffers are sized by the caller via scan_tmp_words.
+size_t scan_tmp_words(int64_t n);
+int scan_u32_to_i64(const uint32_t* in, int64_t n, int64_t* out, int64_t* tmp,
+                    cudaStream_t s);
+int scan_popc_to_i64(const uint32_t* words, int64_t n, int64_t* out, int64_t* tmp,
+                     cudaStream_t s);
+
+// bfs_engine.cu
+int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int strategy,
+                 int want_parents);
+int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_out,
+               int64_t* sizes_out, int64_t max_levels, int64_t* hw_out, bfb_run_stats* st);
+int engine_copy_levels(bfb_ctx* ctx, uint32_t* out);
+int engine_copy_parents(bfb_ctx* ctx, int64_t* out);
+int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs);
+void engine_release(bfb_ctx* ctx);
+
+// schedule (capi.cu)
+int make_schedule(int cn, int fanout, int strategy, std::vector<std::vector<std::vector<int>>>& out);
+
+}  // namespace bfb

@@ -1,0 +1,839 @@
+// ButterFly BFS engine on device: Alg. 2.
+//
+// Per level and per node g (a "part", one per GPU in production, several per
+// GPU for testing):
+//   phase 1  k_expand        edge-balanced top-down expansion of q_local[g]
+//                            (load-balanced search over 2048-edge tiles;
+//                            visited probe + red.or claim; parent write)
+//   phase 2  per round i of the butterfly schedule:
+//            k_publish       snapshot q_global_next[g] as the bitmap
+//                            visited ^ start (round-start snapshot)
+//            k_account       RunStats accounting from the snapshot sizes
+//            k_merge         OR each scheduled source's snapshot into g's
+//                            visited bitmap (check-and-set)
+//   commit   k_commit_owned  new = visited & ~start over g's owned words:
+//                            level writes, start := visited, and the next
+//                            q_local (ascending) with its degree prefix and
+//                            tile starts, via a single-pass decoupled
+//                            look-back scan; frontier count for termination
+//            k_commit_rest   the same level/start update for the other words
+// The synchronized frontier is the bitmap difference; the queue form of
+// q_global is never materialised, so no queue-append atomics exist.
+#include <algorithm>
+#include <cstring>
+
+#include "bfb_device.cuh"
+#include "bfb_internal.cuh"
+
+namespace bfb {
+namespace {
+
+constexpr int kExpandBlock = 256;
+constexpr int kExpandItems = 8;
+constexpr int64_t kTile = (int64_t)kExpandBlock * kExpandItems;  // edges per tile
+constexpr int kCommitBlock = 256;
+constexpr int kCommitWords = 4;                                   // per thread (uint4)
+constexpr int64_t kWordsPerCommitBlock = (int64_t)kCommitBlock * kCommitWords;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+struct PartView {
+  int64_t lo, hi, wlo, whi, nwords;
+  uint32_t* visited;
+  uint32_t* start;
+  uint32_t* level;
+  uint32_t* parent;
+  uint32_t* pub;
+  uint32_t* q_v;
+  int64_t* q_pre;
+  int64_t* q_row;
+  uint32_t* tile_vstart;
+  uint64_t* scan_state;
+  PartCounters* ctr;
+};
+
+PartView view_of(bfb_ctx* ctx, Part& p) {
+  PartView v;
+  v.lo = p.lo;
+  v.hi = p.hi;
+  v.wlo = p.wlo;
+  v.whi = p.whi;
+  v.nwords = (ctx->g.n + 31) / 32;
+  v.visited = p.visited.p;
+  v.start = p.start.p;
+  v.level = p.level.p;
+  v.parent = p.parent.p;
+  v.pub = p.pub.p;
+  v.q_v = p.q_v.p;
+  v.q_pre = p.q_pre.p;
+  v.q_row = p.q_row.p;
+  v.tile_vstart = p.tile_vstart.p;
+  v.scan_state = p.scan_state.p;
+  v.ctr = p.ctr.p;
+  return v;
+}
+
+// ----------------------------------------------------------------- init ---
+__global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root, int owner,
+                       RunCounters* run) {
+  const int64_t w = root >> 5;
+  const uint32_t b = 1u << (root & 31);
+  if (threadIdx.x == 0) {
+    v.visited[w] = b;
+    v.start[w] = b;
+    v.level[root] = 0;
+    if (v.parent) v.parent[root] = (uint32_t)root;
+    PartCounters c{};
+    if (owner) {
+      int64_t d = off[root + 1] - off[root];
+      v.q_v[0] = (uint32_t)root;
+      v.q_pre[0] = 0;
+      v.q_row[0] = off[root];
+      c.q_count = 1;
+      c.q_edges = d;
+      atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)d);
+    }
+    *v.ctr = c;
+  }
+  if (owner) {
+    int64_t d = off[root + 1] - off[root];
+    int64_t nt = (d + kTile - 1) / kTile;
+    for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) v.tile_vstart[t] = 0;
+  }
+}
+
+// ------------------------------------------------------------ phase 1 ----
+template <bool kParents>
+__global__ void __launch_bounds__(kExpandBlock) k_expand(PartView v,
+                                                         const uint32_t* __restrict__ adj) {
+  __shared__ int64_t s_pre[kTile + 1];
+  __shared__ int64_t s_row[kTile + 1];
+  __shared__ uint32_t s_v[kParents ? kTile + 1 : 1];
+  const int64_t T = v.ctr->q_edges;
+  if (T == 0) return;
+  const int64_t qc = v.ctr->q_count;
+  const int64_t ntiles = (T + kTile - 1) / kTile;
+  uint32_t* __restrict__ visited = v.visited;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * kTile;
+    const int64_t e1 = min(e0 + kTile, T);
+    const int64_t vs = v.tile_vstart[t];
+    const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
+    const int nseg = (int)(ve - vs + 1);
+    for (int k = threadIdx.x; k < nseg; k += kExpandBlock) {
+      s_pre[k] = v.q_pre[vs + k];
+      s_row[k] = v.q_row[vs + k];
+      if (kParents) s_v[k] = v.q_v[vs + k];
+    }
+    __syncthreads();
+    uint32_t u[kExpandItems];
+    int seg[kExpandItems];
+#pragma unroll
+    for (int it = 0; it < kExpandItems; ++it) {
+      const int64_t e = e0 + (int64_t)it * kExpandBlock + threadIdx.x;
+      seg[it] = -1;
+      if (e < e1) {
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+          int mid = (lo + hi + 1) >> 1;
+          if (s_pre[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        seg[it] = lo;
+        u[it] = ld_stream_u32(adj + s_row[lo] + (e - s_pre[lo]));
+      }
+    }
+    uint32_t wv[kExpandItems];
+#pragma unroll
+    for (int it = 0; it < kExpandItems; ++it)
+      if (seg[it] >= 0) wv[it] = visited[u[it] >> 5];
+#pragma unroll
+    for (int it = 0; it < kExpandItems; ++it) {
+      if (seg[it] >= 0) {
+        const uint32_t bit = 1u << (u[it] & 31);
+        if (!(wv[it] & bit)) {
+          atomicOr(&visited[u[it] >> 5], bit);
+          if (kParents) v.parent[u[it]] = s_v[seg[it]];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ phase 2 ----
+__global__ void k_publish(PartView v, int parity) {
+  int64_t cnt = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < v.nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t p = v.visited[w] & ~v.start[w];
+    v.pub[w] = p;
+    cnt += __popc(p);
+  }
+  __shared__ int64_t red[32];
+  cnt = block_sum_i64(cnt, red);
+  if (threadIdx.x == 0 && cnt)
+    atomicAdd((unsigned long long*)&v.ctr->pub_count[parity], (unsigned long long)cnt);
+}
+
+struct RoundDesc {
+  const int32_t* pair_dst;   // per pair: receiving node
+  const int32_t* pair_src;   // per pair: source node
+  const int32_t* node_first; // per node: first pair index (CN+1 entries)
+  int npairs;
+  int num_nodes;
+};
+
+// One block.  Snapshot sizes live in pub_count[round parity] so a round can
+// zero the other parity for the next one.
+__global__ void k_account(RoundDesc rd, PartCounters** ctrs, RunCounters* run, int64_t* high_water,
+                          int parity, int64_t bytes_per_transfer) {
+  for (int g = threadIdx.x; g < rd.num_nodes; g += blockDim.x) {
+    int64_t in = 0, msgs = 0;
+    for (int p = rd.node_first[g]; p < rd.node_first[g + 1]; ++p) {
+      PartCounters* c = ctrs[rd.pair_src[p]];
+      int64_t k = c->pub_count[parity];
+      if (k > 0) {  // empty-buffer suppression
+        ++msgs;
+        in += k;
+      }
+    }
+    if (msgs) {
+      atomicAdd((unsigned long long*)&run->remote_messages, (unsigned long long)msgs);
+      atomicAdd((unsigned long long*)&run->remote_vertices, (unsigned long long)in);
+      atomicAdd((unsigned long long*)&run->exchange_bytes,
+                (unsigned long long)(msgs * bytes_per_transfer));
+    }
+    if (in > high_water[g]) high_water[g] = in;
+  }
+}
+
+__global__ void k_zero_parity(PartCounters** ctrs, int num_nodes, int parity) {
+  for (int g = threadIdx.x; g < num_nodes; g += blockDim.x) {
+    ctrs[g]->pub_count[parity] = 0;
+  }
+}
+
+__global__ void k_merge(RoundDesc rd, uint32_t* const* pubs, uint32_t* const* visiteds,
+                        PartCounters** ctrs, int parity, int64_t nwords) {
+  const int p = blockIdx.y;
+  const int src = rd.pair_src[p];
+  const PartCounters* c = ctrs[src];
+  if (c->pub_count[parity] == 0) return;
+  const uint32_t* __restrict__ pub = pubs[src];
+  uint32_t* vis = visiteds[rd.pair_dst[p]];
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t s = pub[w];
+    if (s) {
+      uint32_t nb = s & ~vis[w];
+      if (nb) atomicOr(&vis[w], nb);
+    }
+  }
+}
+
+// ------------------------------------------------------------- commit ----
+__global__ void k_commit_prep(PartCounters** ctrs, int num_nodes, uint64_t* const* scan_states,
+                              const int64_t* scan_words) {
+  for (int g = 0; g < num_nodes; ++g) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctrs[g]->frontier = 0;
+      ctrs[g]->ticket = 0;
+      ctrs[g]->q_count = 0;
+      ctrs[g]->q_edges = 0;
+    }
+    uint64_t* st = scan_states[g];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < scan_words[g];
+         i += (int64_t)gridDim.x * blockDim.x)
+      st[i] = 0;
+  }
+}
+
+__device__ __forceinline__ void lb_publish(uint64_t* st, int64_t bid, uint64_t flag, int64_t cnt,
+                                           int64_t deg) {
+  volatile uint64_t* s = st + 3 * bid;
+  s[1] = (uint64_t)cnt;
+  s[2] = (uint64_t)deg;
+  __threadfence();
+  s[0] = flag;
+}
+
+__global__ void __launch_bounds__(kCommitBlock) k_commit_owned(PartView v,
+                                                               const int64_t* __restrict__ off,
+                                                               uint32_t next_level,
+                                                               RunCounters* run) {
+  __shared__ int64_t s_bid;
+  __shared__ int64_t wsum[33];
+  __shared__ int64_t s_excl_cnt, s_excl_deg;
+  __shared__ int64_t red[32];
+  if (threadIdx.x == 0) s_bid = atomicAdd(&v.ctr->ticket, 1u);
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t wbase = (v.wlo & ~(int64_t)(kCommitWords - 1)) + bid * kWordsPerCommitBlock;
+  const int64_t nblocks =
+      (v.whi - (v.wlo & ~(int64_t)(kCommitWords - 1)) + kWordsPerCommitBlock - 1) /
+      kWordsPerCommitBlock;
+  const int64_t w0 = wbase + (int64_t)threadIdx.x * kCommitWords;
+  uint32_t nb[kCommitWords], vis[kCommitWords];
+  {
+    uint4 a = make_uint4(0, 0, 0, 0), s = make_uint4(0, 0, 0, 0);
+    if (w0 < v.whi) {
+      a = *reinterpret_cast<const uint4*>(v.visited + w0);
+      s = *reinterpret_cast<const uint4*>(v.start + w0);
+    }
+    vis[0] = a.x; vis[1] = a.y; vis[2] = a.z; vis[3] = a.w;
+    nb[0] = a.x & ~s.x; nb[1] = a.y & ~s.y; nb[2] = a.z & ~s.z; nb[3] = a.w & ~s.w;
+  }
+  int64_t cnt = 0, deg = 0, fr = 0;
+  uint32_t own[kCommitWords];
+#pragma unroll
+  for (int j = 0; j < kCommitWords; ++j) {
+    const int64_t w = w0 + j;
+    if (w < v.wlo || w >= v.whi) {
+      nb[j] = 0;
+      own[j] = 0;
+      continue;
+    }
+    uint32_t mask = 0xFFFFFFFFu;
+    const int64_t vb = w << 5;
+    if (vb < v.lo) mask &= 0xFFFFFFFFu << (v.lo - vb);
+    if (vb + 32 > v.hi) mask &= (v.hi - vb) >= 32 ? 0xFFFFFFFFu : ((1u << (v.hi - vb)) - 1u);
+    own[j] = nb[j] & mask;
+    fr += __popc(nb[j]);
+    cnt += __popc(own[j]);
+    uint32_t x = own[j];
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      const int64_t u = vb + b;
+      deg += off[u + 1] - off[u];
+    }
+  }
+  int64_t tot_cnt, tot_deg;
+  const int64_t ex_cnt = block_exclusive_i64(cnt, wsum, &tot_cnt);
+  const int64_t ex_deg = block_exclusive_i64(deg, wsum, &tot_deg);
+  if (threadIdx.x == 0) {
+    int64_t pc = 0, pd = 0;
+    if (bid == 0) {
+      lb_publish(v.scan_state, 0, 2, tot_cnt, tot_deg);
+    } else {
+      lb_publish(v.scan_state, bid, 1, tot_cnt, tot_deg);
+      int64_t j = bid - 1;
+      while (true) {
+        volatile uint64_t* s = v.scan_state + 3 * j;
+        uint64_t f;
+        do { f = s[0]; } while (f == 0);
+        __threadfence();
+        pc += (int64_t)s[1];
+        pd += (int64_t)s[2];
+        if (f == 2) break;
+        --j;
+      }
+      lb_publish(v.scan_state, bid, 2, pc + tot_cnt, pd + tot_deg);
+    }
+    s_excl_cnt = pc;
+    s_excl_deg = pd;
+    if (bid == nblocks - 1) {
+      v.ctr->q_count = pc + tot_cnt;
+      v.ctr->q_edges = pd + tot_deg;
+      atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)(pd + tot_deg));
+    }
+  }
+  __syncthreads();
+  int64_t pos = s_excl_cnt + ex_cnt;
+  int64_t epre = s_excl_deg + ex_deg;
+#pragma unroll
+  for (int j = 0; j < kCommitWords; ++j) {
+    const int64_t w = w0 + j;
+    if (w < v.wlo || w >= v.whi) continue;
+    const int64_t vb = w << 5;
+    uint32_t x = nb[j];
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      const int64_t u = vb + b;
+      v.level[u] = next_level;
+      if ((own[j] >> b) & 1u) {
+        const int64_t r0 = off[u], d = off[u + 1] - r0;
+        v.q_v[pos] = (uint32_t)u;
+        v.q_pre[pos] = epre;
+        v.q_row[pos] = r0;
+        for (int64_t t = (epre + kTile - 1) / kTile; t * kTile < epre + d; ++t)
+          v.tile_vstart[t] = (uint32_t)pos;
+        ++pos;
+        epre += d;
+      }
+    }
+    v.start[w] = vis[j];
+  }
+  fr = block_sum_i64(fr, red);
+  if (threadIdx.x == 0 && fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+}
+
+__global__ void k_commit_rest(PartView v, uint32_t next_level) {
+  int64_t fr = 0;
+  const int64_t span = v.nwords - (v.whi - v.wlo);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < span;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i < v.wlo ? i : i + (v.whi - v.wlo);
+    const uint32_t a = v.visited[w];
+    uint32_t x = a & ~v.start[w];
+    if (!x) continue;
+    fr += __popc(x);
+    const int64_t vb = w << 5;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      v.level[vb + b] = next_level;
+    }
+    v.start[w] = a;
+  }
+  __shared__ int64_t red[32];
+  fr = block_sum_i64(fr, red);
+  if (threadIdx.x == 0 && fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+}
+
+// ------------------------------------------------------------ outputs ----
+__global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n, uint32_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t best = kNone;
+    for (int g = 0; g < num_nodes; ++g) best = min(best, parents[g][i]);
+    out[i] = best;
+  }
+}
+
+// Certificate + parent validity, warp per vertex.
+__global__ void k_validate(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                           int64_t n, const uint32_t* __restrict__ level,
+                           const uint32_t* __restrict__ parent, int64_t root, unsigned* err) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t lu = level[u];
+    unsigned e = 0;
+    bool pred = false;
+    for (int64_t j = off[u] + lane; j < off[u + 1]; j += 32) {
+      const uint32_t lv = level[adj[j]];
+      if ((lu == kNone) != (lv == kNone)) e |= 2u;
+      else if (lu != kNone) {
+        const int64_t dl = (int64_t)lu - (int64_t)lv;
+        if (dl > 1 || dl < -1) e |= 4u;
+        if (lv + 1 == lu) pred = true;
+      }
+    }
+    e |= __reduce_or_sync(0xffffffffu, e);
+    pred = __any_sync(0xffffffffu, pred);
+    if (lane == 0) {
+      if (u == root) {
+        if (lu != 0) e |= 1u;
+        if (parent && parent[u] != (uint32_t)root) e |= 16u;
+      } else if (lu != kNone) {
+        if (!pred) e |= 8u;
+        if (parent) {
+          const uint32_t p = parent[u];
+          if (p == kNone || (int64_t)p >= n || level[p] + 1 != lu) {
+            e |= 16u;
+          } else {
+            int64_t lo = off[p], hi = off[p + 1];
+            while (lo < hi) {
+              int64_t mid = (lo + hi) >> 1;
+              if (adj[mid] < (uint32_t)u) lo = mid + 1; else hi = mid;
+            }
+            if (lo >= off[p + 1] || adj[lo] != (uint32_t)u) e |= 16u;
+          }
+        }
+      } else if (parent && parent[u] != kNone) {
+        e |= 16u;
+      }
+      if (e) atomicOr(err, e);
+    }
+  }
+}
+
+unsigned grid_cap(int64_t work, int block, int num_sms, int per_sm = 8) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = (int64_t)num_sms * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+// Device-side tables built at setup (pointer arrays indexed by node, the
+// butterfly rounds as (dst, src) pair lists) and the timing events.
+struct EngineTables {
+  DevBuf<uint32_t*> pubs, visiteds, parents;
+  DevBuf<PartCounters*> ctrs;
+  DevBuf<uint64_t*> scan_states;
+  DevBuf<int64_t> scan_words;
+  std::vector<DevBuf<int32_t>> round_tables;
+  std::vector<RoundDesc> rounds;
+  DevBuf<uint32_t> parents_final;  // assembled output parents when num_parts > 1
+  int64_t scan_words_max = 0;
+  cudaEvent_t ev[6] = {};
+  ~EngineTables() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+void engine_release(bfb_ctx* ctx) {
+  ctx->parts.clear();
+  ctx->run.release();
+  ctx->high_water.release();
+  ctx->engine_ready = false;
+  ctx->have_run = false;
+  if (ctx->pinned) {
+    cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+  }
+  delete ctx->tables;
+  ctx->tables = nullptr;
+}
+
+int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int strategy,
+                 int want_parents) {
+  if (!ctx->g.valid) return fail(BFB_ERR_STATE, "no graph loaded");
+  const int64_t n = ctx->g.n;
+  if (parts < 1) return fail(BFB_ERR_PARTITION, "num_parts must be >= 1");
+  if (bounds[0] != 0 || bounds[parts] != n)
+    return fail(BFB_ERR_PARTITION, "partition does not match graph");
+  for (int g = 0; g < parts; ++g)
+    if (bounds[g + 1] < bounds[g]) return fail(BFB_ERR_PARTITION, "partition does not match graph");
+  if (strategy != BFB_STRATEGY_BUTTERFLY && strategy != BFB_STRATEGY_ALL2ALL)
+    return fail(BFB_ERR_INVALID, "unknown strategy");
+  if (fanout < 1) return fail(BFB_ERR_FANOUT, "fanout must be >= 1");
+  if (fanout > parts) return fail(BFB_ERR_FANOUT, "fanout exceeds num_nodes");
+  engine_release(ctx);
+  BFB_TRY(make_schedule(parts, fanout, strategy, ctx->schedule));
+  ctx->num_parts = parts;
+  ctx->fanout = fanout;
+  ctx->strategy = strategy;
+  ctx->want_parents = want_parents ? 1 : 0;
+  ctx->bounds.assign(bounds, bounds + parts + 1);
+  ctx->tables = new EngineTables();
+  EngineTables* D = ctx->tables;
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t nwords_pad = (nwords + kWordsPerCommitBlock - 1) / kWordsPerCommitBlock *
+                                 kWordsPerCommitBlock + kWordsPerCommitBlock;
+  std::vector<int64_t> off_h(parts + 1);
+  {
+    // owned edge counts: offsets at the boundaries
+    for (int g = 0; g <= parts; ++g)
+      BFB_CUDA(cudaMemcpy(&off_h[g], ctx->g.offsets.p + bounds[g], sizeof(int64_t),
+                          cudaMemcpyDeviceToHost));
+  }
+  ctx->parts.resize(parts);
+  std::vector<uint32_t*> pubs(parts), viss(parts), pars(parts);
+  std::vector<PartCounters*> ctrs(parts);
+  std::vector<uint64_t*> sstates(parts);
+  std::vector<int64_t> swords(parts);
+  for (int g = 0; g < parts; ++g) {
+    Part& p = ctx->parts[g];
+    p.lo = bounds[g];
+    p.hi = bounds[g + 1];
+    p.wlo = p.lo >> 5;
+    p.whi = (p.hi + 31) >> 5;
+    if (p.hi == p.lo) p.whi = p.wlo;  // empty part owns no words
+    p.owned_edges = off_h[g + 1] - off_h[g];
+    p.tile_cap = (p.owned_edges + kTile - 1) / kTile + 2;
+    const int64_t owned = p.hi - p.lo;
+    BFB_TRY(p.visited.alloc(nwords_pad));
+    BFB_TRY(p.start.alloc(nwords_pad));
+    BFB_TRY(p.level.alloc(n + 1));
+    if (want_parents) BFB_TRY(p.parent.alloc(n + 1));
+    if (parts > 1) BFB_TRY(p.pub.alloc(nwords_pad));
+    BFB_TRY(p.q_v.alloc(owned + 1));
+    BFB_TRY(p.q_pre.alloc(owned + 1));
+    BFB_TRY(p.q_row.alloc(owned + 1));
+    BFB_TRY(p.tile_vstart.alloc(p.tile_cap));
+    const int64_t cblocks =
+        (p.whi - (p.wlo & ~(int64_t)(kCommitWords - 1)) + kWordsPerCommitBlock - 1) /
+            kWordsPerCommitBlock + 1;
+    BFB_TRY(p.scan_state.alloc(3 * cblocks));
+    BFB_TRY(p.ctr.alloc(1));
+    BFB_CUDA(cudaMemset(p.visited.p, 0, nwords_pad * sizeof(uint32_t)));
+    BFB_CUDA(cudaMemset(p.start.p, 0, nwords_pad * sizeof(uint32_t)));
+    if (parts > 1) BFB_CUDA(cudaMemset(p.pub.p, 0, nwords_pad * sizeof(uint32_t)));
+    BFB_CUDA(cudaMemset(p.ctr.p, 0, sizeof(PartCounters)));
+    pubs[g] = p.pub.p;
+    viss[g] = p.visited.p;
+    pars[g] = p.parent.p;
+    ctrs[g] = p.ctr.p;
+    sstates[g] = p.scan_state.p;
+    swords[g] = 3 * cblocks;
+    D->scan_words_max = std::max(D->scan_words_max, 3 * cblocks);
+  }
+  BFB_TRY(D->pubs.alloc(parts));
+  BFB_TRY(D->visiteds.alloc(parts));
+  BFB_TRY(D->parents.alloc(parts));
+  BFB_TRY(D->ctrs.alloc(parts));
+  BFB_TRY(D->scan_states.alloc(parts));
+  BFB_TRY(D->scan_words.alloc(parts));
+  BFB_CUDA(cudaMemcpy(D->pubs.p, pubs.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
+  BFB_CUDA(cudaMemcpy(D->visiteds.p, viss.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
+  BFB_CUDA(cudaMemcpy(D->parents.p, pars.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
+  BFB_CUDA(cudaMemcpy(D->ctrs.p, ctrs.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
+  BFB_CUDA(cudaMemcpy(D->scan_states.p, sstates.data(), parts * sizeof(void*),
+                      cudaMemcpyHostToDevice));
+  BFB_CUDA(cudaMemcpy(D->scan_words.p, swords.data(), parts * sizeof(int64_t),
+                      cudaMemcpyHostToDevice));
+  // round tables
+  for (auto& rnd : ctx->schedule) {
+    std::vector<int32_t> dst, src, first(parts + 1, 0);
+    for (int g = 0; g < parts; ++g) {
+      first[g] = (int32_t)dst.size();
+      for (int s : rnd[g]) {
+        dst.push_back(g);
+        src.push_back(s);
+      }
+    }
+    first[parts] = (int32_t)dst.size();
+    DevBuf<int32_t> tab;
+    const int np = (int)dst.size();
+    BFB_TRY(tab.alloc(2 * (size_t)np + parts + 1));
+    if (np) {
+      BFB_CUDA(cudaMemcpy(tab.p, dst.data(), np * sizeof(int32_t), cudaMemcpyHostToDevice));
+      BFB_CUDA(cudaMemcpy(tab.p + np, src.data(), np * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    BFB_CUDA(cudaMemcpy(tab.p + 2 * np, first.data(), (parts + 1) * sizeof(int32_t),
+                        cudaMemcpyHostToDevice));
+    RoundDesc rd;
+    rd.pair_dst = tab.p;
+    rd.pair_src = tab.p + np;
+    rd.node_first = tab.p + 2 * np;
+    rd.npairs = np;
+    rd.num_nodes = parts;
+    D->rounds.push_back(rd);
+    D->round_tables.push_back(std::move(tab));
+  }
+  if (want_parents && parts > 1) BFB_TRY(D->parents_final.alloc(n + 1));
+  BFB_TRY(ctx->run.alloc(1));
+  BFB_TRY(ctx->high_water.alloc(parts));
+  BFB_CUDA(cudaMallocHost(&ctx->pinned, sizeof(int64_t) * (8 + 8 * (size_t)parts)));
+  int occ = 0;
+  if (want_parents)
+    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<true>, kExpandBlock, 0));
+  else
+    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<false>, kExpandBlock, 0));
+  ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
+  for (auto& ev : D->ev) BFB_CUDA(cudaEventCreate(&ev));
+  ctx->engine_ready = true;
+  return BFB_OK;
+}
+
+int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_out,
+               int64_t* sizes_out, int64_t max_levels, int64_t* hw_out, bfb_run_stats* st) {
+  if (!ctx->engine_ready) return fail(BFB_ERR_STATE, "engine not set up");
+  const int64_t n = ctx->g.n;
+  if (root < 0 || root >= n)
+    return fail(BFB_ERR_ROOT, "root " + std::to_string(root) + " out of range [0, " +
+                                  std::to_string(n) + ")");
+  EngineTables* D = ctx->tables;
+  cudaStream_t s = ctx->stream;
+  const int P = ctx->num_parts;
+  const int sms = ctx->num_sms;
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t* off = ctx->g.offsets.p;
+  int64_t launches = 0;
+  double t_expand = 0, t_exchange = 0, t_commit = 0;
+  int64_t expand_launches = 0;
+
+  BFB_CUDA(cudaEventRecord(D->ev[0], s));
+  // init: every node d_local = UNREACHED, d_local[root] = 0
+  BFB_CUDA(cudaMemsetAsync(ctx->run.p, 0, sizeof(RunCounters), s));
+  BFB_CUDA(cudaMemsetAsync(ctx->high_water.p, 0, P * sizeof(int64_t), s));
+  int owner = 0;
+  for (int g = 0; g < P; ++g)
+    if (root >= ctx->bounds[g] && root < ctx->bounds[g + 1]) owner = g;
+  for (int g = 0; g < P; ++g) {
+    Part& p = ctx->parts[g];
+    BFB_CUDA(cudaMemsetAsync(p.visited.p, 0, nwords * sizeof(uint32_t), s));
+    BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
+    BFB_CUDA(cudaMemsetAsync(p.level.p, 0xFF, n * sizeof(uint32_t), s));
+    if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
+    k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), off, root, g == owner ? 1 : 0, ctx->run.p);
+    ++launches;
+  }
+  const int64_t bytes_per_transfer = nwords * (int64_t)sizeof(uint32_t);
+  int64_t level = 0;
+  int64_t nsizes = 0;
+  if (max_levels > 0 && sizes_out) sizes_out[0] = 1;
+  nsizes = 1;
+  int64_t reached = 1;
+  const unsigned small_grid = grid_cap(nwords, 256, sms, 4);
+  while (true) {
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
+    // Phase 1
+    for (int g = 0; g < P; ++g) {
+      PartView v = view_of(ctx, ctx->parts[g]);
+      if (ctx->want_parents)
+        k_expand<true><<<ctx->expand_grid, kExpandBlock, 0, s>>>(v, ctx->g.adj.p);
+      else
+        k_expand<false><<<ctx->expand_grid, kExpandBlock, 0, s>>>(v, ctx->g.adj.p);
+      ++launches;
+      ++expand_launches;
+    }
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[3], s));
+    // Phase 2
+    if (!D->rounds.empty()) {
+      k_zero_parity<<<1, 256, 0, s>>>(D->ctrs.p, P, 0);
+      k_zero_parity<<<1, 256, 0, s>>>(D->ctrs.p, P, 1);
+      launches += 2;
+    }
+    for (size_t r = 0; r < D->rounds.size(); ++r) {
+      const int parity = (int)(r & 1);
+      const RoundDesc& rd = D->rounds[r];
+      for (int g = 0; g < P; ++g) {
+        k_publish<<<small_grid, 256, 0, s>>>(view_of(ctx, ctx->parts[g]), parity);
+        ++launches;
+      }
+      k_account<<<1, 256, 0, s>>>(rd, D->ctrs.p, ctx->run.p, ctx->high_water.p, parity,
+                                  bytes_per_transfer);
+      k_zero_parity<<<1, 256, 0, s>>>(D->ctrs.p, P, parity ^ 1);
+      launches += 2;
+      if (rd.npairs) {
+        dim3 grid(grid_cap(nwords, 256, sms, 2), rd.npairs);
+        k_merge<<<grid, 256, 0, s>>>(rd, D->pubs.p, D->visiteds.p, D->ctrs.p, parity, nwords);
+        ++launches;
+      }
+    }
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[4], s));
+    // Commit: levels, start snapshot, next q_local, frontier count.
+    k_commit_prep<<<grid_cap(D->scan_words_max, 256, sms, 1), 256, 0, s>>>(
+        D->ctrs.p, P, D->scan_states.p, D->scan_words.p);
+    ++launches;
+    const uint32_t next_level = (uint32_t)(level + 1);
+    for (int g = 0; g < P; ++g) {
+      Part& p = ctx->parts[g];
+      PartView v = view_of(ctx, p);
+      if (p.whi > p.wlo) {
+        const int64_t cb = (p.whi - (p.wlo & ~(int64_t)(kCommitWords - 1)) +
+                            kWordsPerCommitBlock - 1) / kWordsPerCommitBlock;
+        k_commit_owned<<<(unsigned)cb, kCommitBlock, 0, s>>>(v, off, next_level, ctx->run.p);
+        ++launches;
+      }
+      if (nwords - (p.whi - p.wlo) > 0) {
+        k_commit_rest<<<small_grid, 256, 0, s>>>(v, next_level);
+        ++launches;
+      }
+    }
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
+    // Termination: node 0's synchronized frontier.
+    BFB_CUDA(cudaMemcpyAsync(ctx->pinned, &ctx->parts[0].ctr.p->frontier, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
+    BFB_CUDA(cudaGetLastError());
+    if (ctx->timing) {
+      float a = 0, b = 0, c = 0;
+      BFB_CUDA(cudaEventElapsedTime(&a, D->ev[2], D->ev[3]));
+      BFB_CUDA(cudaEventElapsedTime(&b, D->ev[3], D->ev[4]));
+      BFB_CUDA(cudaEventElapsedTime(&c, D->ev[4], D->ev[5]));
+      t_expand += a;
+      t_exchange += b;
+      t_commit += c;
+    }
+    const int64_t frontier = ctx->pinned[0];
+    if (frontier == 0) break;
+    if (nsizes < max_levels && sizes_out) sizes_out[nsizes] = frontier;
+    ++nsizes;
+    reached += frontier;
+    ++level;
+    if (level > n) return fail(BFB_ERR_CAPACITY, "level count exceeded |V| (internal error)");
+  }
+  BFB_CUDA(cudaEventRecord(D->ev[1], s));
+  // Parents of the output view: any node's phase-1 claim is a valid parent.
+  const uint32_t* parents_dev = nullptr;
+  if (ctx->want_parents) {
+    if (P == 1) {
+      parents_dev = ctx->parts[0].parent.p;
+    } else {
+      k_parents_min<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(D->parents.p, P, n,
+                                                             D->parents_final.p);
+      parents_dev = D->parents_final.p;
+    }
+  }
+  // Stats
+  RunCounters rc;
+  BFB_CUDA(cudaMemcpyAsync(&rc, ctx->run.p, sizeof(rc), cudaMemcpyDeviceToHost, s));
+  std::vector<int64_t> hw(P);
+  BFB_CUDA(cudaMemcpyAsync(hw.data(), ctx->high_water.p, P * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, s));
+  if (levels_out)
+    BFB_CUDA(cudaMemcpyAsync(levels_out, ctx->parts[0].level.p, n * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, s));
+  BFB_CUDA(cudaStreamSynchronize(s));
+  float elapsed = 0;
+  BFB_CUDA(cudaEventElapsedTime(&elapsed, D->ev[0], D->ev[1]));
+  if (parents_out) {
+    if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
+    std::vector<uint32_t> tmp(n);
+    BFB_CUDA(cudaMemcpy(tmp.data(), parents_dev, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) parents_out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
+  }
+  if (hw_out) std::memcpy(hw_out, hw.data(), P * sizeof(int64_t));
+  ctx->have_run = true;
+  ctx->last_root = root;
+  ctx->last_levels = nsizes;
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->levels = nsizes;
+    st->rounds_executed = nsizes * (int64_t)ctx->schedule.size();
+    st->remote_messages = rc.remote_messages;
+    st->remote_vertices = rc.remote_vertices;
+    st->traversed_edges = rc.traversed_edges;
+    st->reached = reached;
+    int64_t mx = 0;
+    for (auto x : hw) mx = std::max(mx, x);
+    st->buffer_high_water_max = mx;
+    st->exchange_bytes = rc.exchange_bytes;
+    st->elapsed_ms = elapsed;
+    st->expand_ms = t_expand;
+    st->exchange_ms = t_exchange;
+    st->commit_ms = t_commit;
+    st->expand_launches = expand_launches;
+    st->kernel_launches = launches;
+  }
+  // buffer-bound check: incoming <= f * |V|
+  for (auto x : hw)
+    if (x > (int64_t)ctx->fanout * n && ctx->strategy == BFB_STRATEGY_BUTTERFLY)
+      return fail(BFB_ERR_CAPACITY, "buffer bound violated");
+  return BFB_OK;
+}
+
+int engine_copy_levels(bfb_ctx* ctx, uint32_t* out) {
+  if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
+  BFB_CUDA(cudaMemcpy(out, ctx->parts[0].level.p, ctx->g.n * sizeof(uint32_t),
+                      cudaMemcpyDeviceToHost));
+  return BFB_OK;
+}
+
+int engine_copy_parents(bfb_ctx* ctx, int64_t* out) {
+  if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
+  if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
+  EngineTables* D = ctx->tables;
+  const uint32_t* src = ctx->num_parts == 1 ? ctx->parts[0].parent.p : D->parents_final.p;
+  std::vector<uint32_t> tmp(ctx->g.n);
+  BFB_CUDA(cudaMemcpy(tmp.data(), src, ctx->g.n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < ctx->g.n; ++i) out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
+  return BFB_OK;
+}
+
+int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs) {
+  if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
+  EngineTables* D = ctx->tables;
+  const uint32_t* par = nullptr;
+  if (ctx->want_parents) par = ctx->num_parts == 1 ? ctx->parts[0].parent.p : D->parents_final.p;
+  DevBuf<unsigned> err;
+  BFB_TRY(err.alloc(1));
+  BFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(unsigned), ctx->stream));
+  k_validate<<<grid_cap(ctx->g.n * 32, 256, ctx->num_sms, 16), 256, 0, ctx->stream>>>(
+      ctx->g.offsets.p, ctx->g.adj.p, ctx->g.n, ctx->parts[0].level.p, par, root, err.p);
+  unsigned h = 0;
+  BFB_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  BFB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *errs = (int64_t)h;
+  return BFB_OK;
+}
+
+}  // namespace bfb

@@ -1,0 +1,190 @@
+"""Device-resident graph handle over the C ABI (one bfb_ctx per graph).
+
+A ``DeviceGraph`` owns a CSR in HBM (built on device or uploaded) and the
+engine buffers of the last ``setup``; nothing here falls back to the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_int64, c_void_p
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr
+
+
+class DeviceGraph:
+    """CSR graph resident on one GPU plus its ButterFly BFS engine state."""
+
+    def __init__(self, device=0):
+        lib = _lib.load()
+        h = c_void_p()
+        check(lib.bfb_create(byref(h), int(device)))
+        self._h = h
+        self.device = int(device)
+        self._engine_key = None
+        self._n = self._m = self._maxdeg = None
+
+    # -- lifetime ------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.load().bfb_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("DeviceGraph is closed")
+        return self._h
+
+    # -- construction ----------------------------------------------------------
+    @classmethod
+    def from_rmat(cls, scale, edge_factor, seed, probs=None, device=0):
+        """generate_rmat -> symmetrize -> build_csr fused on device."""
+        from .graphs import RMAT_PROBS, rmat_device_args
+
+        state, inc, thr = rmat_device_args(scale, edge_factor, seed, probs or RMAT_PROBS)
+        dg = cls(device)
+        check(_lib.load().bfb_graph_from_rmat(dg.handle, int(scale), int(edge_factor),
+                                              ptr(state, ctypes.c_uint64), ptr(inc, ctypes.c_uint64),
+                                              ptr(thr, ctypes.c_uint64)))
+        dg._refresh()
+        return dg
+
+    @classmethod
+    def from_edges(cls, edges, num_vertices, symmetrize, device=0):
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+        dg = cls(device)
+        check(_lib.load().bfb_graph_from_edges(dg.handle, int(num_vertices),
+                                               ptr(e, ctypes.c_uint32), int(e.shape[0]),
+                                               1 if symmetrize else 0))
+        dg._refresh()
+        return dg
+
+    @classmethod
+    def from_csr(cls, offsets, adjacency, device=0):
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        adj = np.ascontiguousarray(adjacency, dtype=np.uint32)
+        dg = cls(device)
+        check(_lib.load().bfb_graph_load_csr(dg.handle, off.size - 1, adj.size,
+                                             ptr(off, ctypes.c_int64), ptr(adj, ctypes.c_uint32)))
+        dg._refresh()
+        return dg
+
+    def _refresh(self):
+        n, m, md = c_int64(), c_int64(), c_int64()
+        check(_lib.load().bfb_graph_info(self.handle, byref(n), byref(m), byref(md)))
+        self._n, self._m, self._maxdeg = n.value, m.value, md.value
+
+    # -- queries ---------------------------------------------------------------
+    @property
+    def num_vertices(self):
+        return self._n
+
+    @property
+    def num_edges(self):
+        return self._m
+
+    @property
+    def max_degree(self):
+        return self._maxdeg
+
+    def csr(self):
+        off = np.empty(self._n + 1, dtype=np.int64)
+        adj = np.empty(self._m, dtype=np.uint32)
+        check(_lib.load().bfb_graph_copy_csr(self.handle, ptr(off, ctypes.c_int64),
+                                             ptr(adj, ctypes.c_uint32)))
+        return off, adj
+
+    def offsets(self):
+        off = np.empty(self._n + 1, dtype=np.int64)
+        check(_lib.load().bfb_graph_copy_csr(self.handle, ptr(off, ctypes.c_int64), None))
+        return off
+
+    def adjacency(self):
+        adj = np.empty(self._m, dtype=np.uint32)
+        check(_lib.load().bfb_graph_copy_csr(self.handle, None, ptr(adj, ctypes.c_uint32)))
+        return adj
+
+    def edges(self):
+        out = np.empty((self._m, 2), dtype=np.uint32)
+        check(_lib.load().bfb_graph_copy_edges(self.handle, ptr(out, ctypes.c_uint32)))
+        return out
+
+    def partition_1d(self, num_parts):
+        b = np.empty(int(num_parts) + 1, dtype=np.int64)
+        check(_lib.load().bfb_partition_1d(self.handle, int(num_parts), ptr(b, ctypes.c_int64)))
+        return b
+
+    def count_nonisolated(self):
+        c = c_int64()
+        check(_lib.load().bfb_count_nonisolated(self.handle, byref(c)))
+        return c.value
+
+    def select_nonisolated(self, ranks):
+        r = np.ascontiguousarray(ranks, dtype=np.int64)
+        out = np.empty(r.size, dtype=np.int64)
+        check(_lib.load().bfb_select_nonisolated(self.handle, ptr(r, ctypes.c_int64), r.size,
+                                                 ptr(out, ctypes.c_int64)))
+        return out
+
+    # -- engine ----------------------------------------------------------------
+    def setup(self, boundaries, fanout=1, strategy="butterfly", parents=False):
+        """Allocate the per-node engine buffers once."""
+        b = np.ascontiguousarray(boundaries, dtype=np.int64)
+        if strategy not in _lib.STRATEGY:
+            raise ValueError(f"unknown strategy {strategy!r}")
+        key = (tuple(b.tolist()), int(fanout), _lib.STRATEGY[strategy], bool(parents))
+        if key == self._engine_key:
+            return
+        self._engine_key = None
+        check(_lib.load().bfb_engine_setup(self.handle, b.size - 1, ptr(b, ctypes.c_int64),
+                                           int(fanout), _lib.STRATEGY[strategy],
+                                           1 if parents else 0))
+        self._engine_key = key
+
+    @property
+    def num_parts(self):
+        return len(self._engine_key[0]) - 1 if self._engine_key else 0
+
+    def set_timing(self, enabled):
+        check(_lib.load().bfb_set_timing(self.handle, 1 if enabled else 0))
+
+    def bfs(self, root, levels=True, parents=False, max_levels=4096):
+        """One BFS on the configured engine.  Returns (levels|None,
+        parents|None, frontier_sizes, RunStatsC, buffer_high_water)."""
+        if self._engine_key is None:
+            raise RuntimeError("engine not set up")
+        lv = np.empty(self._n, dtype=np.uint32) if levels else None
+        pa = np.empty(self._n, dtype=np.int64) if parents else None
+        sizes = np.zeros(max_levels, dtype=np.int64)
+        hw = np.zeros(self.num_parts, dtype=np.int64)
+        st = _lib.RunStatsC()
+        check(_lib.load().bfb_bfs(self.handle, int(root), ptr(lv, ctypes.c_uint32),
+                                  ptr(pa, ctypes.c_int64), ptr(sizes, ctypes.c_int64), max_levels,
+                                  ptr(hw, ctypes.c_int64), byref(st)))
+        return lv, pa, sizes[:min(st.levels, max_levels)].tolist(), st, hw
+
+    def levels(self):
+        out = np.empty(self._n, dtype=np.uint32)
+        check(_lib.load().bfb_copy_levels(self.handle, ptr(out, ctypes.c_uint32)))
+        return out
+
+    def parents(self):
+        out = np.empty(self._n, dtype=np.int64)
+        check(_lib.load().bfb_copy_parents(self.handle, ptr(out, ctypes.c_int64)))
+        return out
+
+    def validate(self, root):
+        """Device certificate of the last run: 0 = valid."""
+        e = c_int64()
+        check(_lib.load().bfb_validate(self.handle, int(root), byref(e)))
+        return e.value
