@@ -83,6 +83,10 @@ int bfb_create(bfb_ctx** ctx_out, int device);
 void bfb_destroy(bfb_ctx* ctx);
 /* Record per-phase CUDA events inside bfb_bfs (fills *_ms of bfb_run_stats). */
 int bfb_set_timing(bfb_ctx* ctx, int enabled);
+/* Device-side bracket timer on the context's stream: start records a CUDA
+ * event, stop records another, synchronizes and returns the elapsed ms. */
+int bfb_timer_start(bfb_ctx* ctx);
+int bfb_timer_stop(bfb_ctx* ctx, double* elapsed_ms_out);
 
 /* ---- graph-core on device (graphs.py) ------------------------------------ */
 /* generate_rmat (graphs.py:254-285): raw edges to a HOST buffer of 2*m uint32

@@ -61,6 +61,8 @@ _SIGNATURES = {
     "bfb_create": (c_int, [POINTER(c_void_p), c_int]),
     "bfb_destroy": (None, [c_void_p]),
     "bfb_set_timing": (c_int, [c_void_p, c_int]),
+    "bfb_timer_start": (c_int, [c_void_p]),
+    "bfb_timer_stop": (c_int, [c_void_p, POINTER(c_double)]),
     "bfb_rmat_edges": (c_int, [c_void_p, c_int, c_int64, _U64P, _U64P, _U64P, _U32P]),
     "bfb_graph_from_rmat": (c_int, [c_void_p, c_int, c_int64, _U64P, _U64P, _U64P]),
     "bfb_graph_from_edges": (c_int, [c_void_p, c_int64, _U32P, c_int64, c_int]),

@@ -147,8 +147,6 @@ struct PartCounters {
   int64_t q_edges;      // sum of degrees over q_local
   int64_t frontier;     // |synchronized next frontier| counted at commit
   int64_t pub_count[2]; // published snapshot size, by round parity (phase 2)
-  uint32_t ticket;      // dynamic block ids for the look-back scan
-  uint32_t pad;
 };
 
 // Device-resident run statistics (RunStats).
@@ -175,7 +173,7 @@ struct Part {
   DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local
   DevBuf<int64_t> q_row;           // offsets[v] of each q_local vertex
   DevBuf<uint32_t> tile_vstart;    // q_local index owning edge t*TILE
-  DevBuf<uint64_t> scan_state;     // look-back tile status (2 words / tile)
+  DevBuf<int64_t> block_sums;      // commit reduce/scan: (count, degree) per block
   DevBuf<PartCounters> ctr;
 };
 
@@ -207,6 +205,7 @@ struct bfb_ctx {
   int64_t last_root = -1;
   int64_t last_levels = 0;
   int64_t launches = 0;
+  cudaEvent_t timer[2] = {nullptr, nullptr};
 };
 
 namespace bfb {

@@ -20,6 +20,7 @@
 // The synchronized frontier is the bitmap difference; the queue form of
 // q_global is never materialised, so no queue-append atomics exist.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "bfb_device.cuh"
@@ -32,8 +33,12 @@ constexpr int kExpandBlock = 256;
 constexpr int kExpandItems = 8;
 constexpr int64_t kTile = (int64_t)kExpandBlock * kExpandItems;  // edges per tile
 constexpr int kCommitBlock = 256;
-constexpr int kCommitWords = 4;                                   // per thread (uint4)
-constexpr int64_t kWordsPerCommitBlock = (int64_t)kCommitBlock * kCommitWords;
+constexpr int64_t kWordsPerCommitBlock = 1024;                    // 32768 vertices
+
+// Commit blocks of a part: word range [wlo & ~31, whi) in 1024-word blocks.
+__host__ __device__ inline int64_t commit_blocks(int64_t wlo, int64_t whi) {
+  return (whi - (wlo & ~(int64_t)31) + kWordsPerCommitBlock - 1) / kWordsPerCommitBlock;
+}
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct PartView {
@@ -47,7 +52,7 @@ struct PartView {
   int64_t* q_pre;
   int64_t* q_row;
   uint32_t* tile_vstart;
-  uint64_t* scan_state;
+  int64_t* block_sums;
   PartCounters* ctr;
 };
 
@@ -67,7 +72,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.q_pre = p.q_pre.p;
   v.q_row = p.q_row.p;
   v.tile_vstart = p.tile_vstart.p;
-  v.scan_state = p.scan_state.p;
+  v.block_sums = p.block_sums.p;
   v.ctr = p.ctr.p;
   return v;
 }
@@ -102,43 +107,94 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
 }
 
 // ------------------------------------------------------------ phase 1 ----
+// One 2048-edge tile per block iteration (load-balanced search).  The tile's
+// frontier segment is staged in shared memory as adjacency bases (row start
+// minus edge prefix).  Each edge finds its vertex either by binary search over
+// the segments' first edges (few segments: hub tiles) or through an owner map
+// built by scattering segment starts and a block max-scan (many segments:
+// low-degree tiles).  Small staging keeps more of the unified L1 for probes.
+constexpr int kSearchMax = 16;
+
 template <bool kParents>
 __global__ void __launch_bounds__(kExpandBlock) k_expand(PartView v,
                                                          const uint32_t* __restrict__ adj) {
-  __shared__ int64_t s_pre[kTile + 1];
-  __shared__ int64_t s_row[kTile + 1];
+  __shared__ int32_t s_idx[kTile + 1];   // segment first edges (search) or owner map
+  __shared__ int64_t s_base[kTile + 1];
   __shared__ uint32_t s_v[kParents ? kTile + 1 : 1];
+  __shared__ int32_t s_wmax[kExpandBlock / 32];
   const int64_t T = v.ctr->q_edges;
   if (T == 0) return;
   const int64_t qc = v.ctr->q_count;
   const int64_t ntiles = (T + kTile - 1) / kTile;
   uint32_t* __restrict__ visited = v.visited;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t e0 = t * kTile;
-    const int64_t e1 = min(e0 + kTile, T);
+    const int span = (int)min((int64_t)kTile, T - e0);
     const int64_t vs = v.tile_vstart[t];
     const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
     const int nseg = (int)(ve - vs + 1);
+    const bool use_map = nseg > kSearchMax;
+    if (use_map) {
+      for (int k = threadIdx.x; k < kTile; k += kExpandBlock) s_idx[k] = 0;
+      __syncthreads();
+    }
     for (int k = threadIdx.x; k < nseg; k += kExpandBlock) {
-      s_pre[k] = v.q_pre[vs + k];
-      s_row[k] = v.q_row[vs + k];
+      const int64_t pre = v.q_pre[vs + k];
+      s_base[k] = v.q_row[vs + k] - pre;
       if (kParents) s_v[k] = v.q_v[vs + k];
+      if (use_map) {
+        const int64_t r = pre - e0;
+        if (r > 0 && r < span) s_idx[r] = k;
+      } else {
+        s_idx[k] = (int32_t)max(pre - e0, (int64_t)INT32_MIN);
+      }
     }
     __syncthreads();
+    if (use_map) {  // inclusive max-scan of the owner map, 8 entries per thread
+      constexpr int kPer = kTile / kExpandBlock;
+      int32_t loc[kPer];
+      int32_t run = 0;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        run = max(run, s_idx[threadIdx.x * kPer + i]);
+        loc[i] = run;
+      }
+      int32_t inc = run;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc = max(inc, o);
+      }
+      if (lane == 31) s_wmax[warp] = inc;
+      __syncthreads();
+      int32_t carry = 0;
+      for (int w = 0; w < warp; ++w) carry = max(carry, s_wmax[w]);
+      const int32_t prev = max(carry, __shfl_up_sync(0xffffffffu, inc, 1) * (lane > 0));
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) s_idx[threadIdx.x * kPer + i] = max(prev, loc[i]);
+      __syncthreads();
+    }
     uint32_t u[kExpandItems];
     int seg[kExpandItems];
 #pragma unroll
     for (int it = 0; it < kExpandItems; ++it) {
-      const int64_t e = e0 + (int64_t)it * kExpandBlock + threadIdx.x;
+      const int r = it * kExpandBlock + threadIdx.x;
       seg[it] = -1;
-      if (e < e1) {
-        int lo = 0, hi = nseg - 1;
-        while (lo < hi) {
-          int mid = (lo + hi + 1) >> 1;
-          if (s_pre[mid] <= e) lo = mid; else hi = mid - 1;
+      if (r < span) {
+        int lo;
+        if (use_map) {
+          lo = s_idx[r];
+        } else {
+          lo = 0;
+          int hi = nseg - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_idx[mid] <= r) lo = mid; else hi = mid - 1;
+          }
         }
         seg[it] = lo;
-        u[it] = ld_stream_u32(adj + s_row[lo] + (e - s_pre[lo]));
+        u[it] = ld_stream_u32(adj + s_base[lo] + e0 + r);
       }
     }
     uint32_t wv[kExpandItems];
@@ -231,141 +287,181 @@ __global__ void k_merge(RoundDesc rd, uint32_t* const* pubs, uint32_t* const* vi
 }
 
 // ------------------------------------------------------------- commit ----
-__global__ void k_commit_prep(PartCounters** ctrs, int num_nodes, uint64_t* const* scan_states,
-                              const int64_t* scan_words) {
-  for (int g = 0; g < num_nodes; ++g) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      ctrs[g]->frontier = 0;
-      ctrs[g]->ticket = 0;
-      ctrs[g]->q_count = 0;
-      ctrs[g]->q_edges = 0;
-    }
-    uint64_t* st = scan_states[g];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < scan_words[g];
-         i += (int64_t)gridDim.x * blockDim.x)
-      st[i] = 0;
+__global__ void k_commit_prep(PartCounters** ctrs, int num_nodes) {
+  for (int g = threadIdx.x; g < num_nodes; g += blockDim.x) {
+    ctrs[g]->frontier = 0;
+    ctrs[g]->q_count = 0;
+    ctrs[g]->q_edges = 0;
   }
 }
 
-__device__ __forceinline__ void lb_publish(uint64_t* st, int64_t bid, uint64_t flag, int64_t cnt,
-                                           int64_t deg) {
-  volatile uint64_t* s = st + 3 * bid;
-  s[1] = (uint64_t)cnt;
-  s[2] = (uint64_t)deg;
-  __threadfence();
-  s[0] = flag;
+__device__ __forceinline__ uint32_t owned_mask(int64_t w, int64_t lo, int64_t hi) {
+  const int64_t vb = w << 5;
+  uint32_t mask = 0xFFFFFFFFu;
+  if (vb < lo) mask = (lo - vb) >= 32 ? 0u : (mask << (lo - vb));
+  if (vb + 32 > hi) mask &= (hi - vb) <= 0 ? 0u : ((hi - vb) >= 32 ? 0xFFFFFFFFu : ((1u << (hi - vb)) - 1u));
+  return mask;
 }
 
+// Commit of the owned words, as reduce (kWrite = false) -> scan -> write
+// (kWrite = true) over 1024-word blocks.  Lane l of a warp holds word
+// (chunk base + l) of each chunk; vertex work then runs with lane = bit, so
+// offsets reads, level writes and queue writes are coalesced.  The reduce
+// pass stores (owned new vertices, their degree sum) per block; the write
+// pass recomputes them and emits q_local in ascending vertex order.
+template <bool kWrite>
 __global__ void __launch_bounds__(kCommitBlock) k_commit_owned(PartView v,
                                                                const int64_t* __restrict__ off,
-                                                               uint32_t next_level,
-                                                               RunCounters* run) {
-  __shared__ int64_t s_bid;
-  __shared__ int64_t wsum[33];
-  __shared__ int64_t s_excl_cnt, s_excl_deg;
+                                                               uint32_t next_level) {
+  constexpr int kWarps = kCommitBlock / 32;
+  constexpr int kChunks = kWordsPerCommitBlock / kCommitBlock;  // words per lane
+  __shared__ int64_t s_wcnt[kWarps], s_wdeg[kWarps];
   __shared__ int64_t red[32];
-  if (threadIdx.x == 0) s_bid = atomicAdd(&v.ctr->ticket, 1u);
-  __syncthreads();
-  const int64_t bid = s_bid;
-  const int64_t wbase = (v.wlo & ~(int64_t)(kCommitWords - 1)) + bid * kWordsPerCommitBlock;
-  const int64_t nblocks =
-      (v.whi - (v.wlo & ~(int64_t)(kCommitWords - 1)) + kWordsPerCommitBlock - 1) /
-      kWordsPerCommitBlock;
-  const int64_t w0 = wbase + (int64_t)threadIdx.x * kCommitWords;
-  uint32_t nb[kCommitWords], vis[kCommitWords];
-  {
-    uint4 a = make_uint4(0, 0, 0, 0), s = make_uint4(0, 0, 0, 0);
-    if (w0 < v.whi) {
-      a = *reinterpret_cast<const uint4*>(v.visited + w0);
-      s = *reinterpret_cast<const uint4*>(v.start + w0);
-    }
-    vis[0] = a.x; vis[1] = a.y; vis[2] = a.z; vis[3] = a.w;
-    nb[0] = a.x & ~s.x; nb[1] = a.y & ~s.y; nb[2] = a.z & ~s.z; nb[3] = a.w & ~s.w;
-  }
-  int64_t cnt = 0, deg = 0, fr = 0;
-  uint32_t own[kCommitWords];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t bid = blockIdx.x;
+  const int64_t wbase = (v.wlo & ~(int64_t)31) + bid * kWordsPerCommitBlock +
+                        (int64_t)warp * (kChunks * 32);
+  uint32_t nb[kChunks], own[kChunks], vis[kChunks];
+  int64_t cnt = 0, fr = 0;
 #pragma unroll
-  for (int j = 0; j < kCommitWords; ++j) {
-    const int64_t w = w0 + j;
-    if (w < v.wlo || w >= v.whi) {
-      nb[j] = 0;
-      own[j] = 0;
-      continue;
+  for (int c = 0; c < kChunks; ++c) {
+    const int64_t w = wbase + c * 32 + lane;
+    const bool in = w >= v.wlo && w < v.whi;
+    const uint32_t a = in ? v.visited[w] : 0u;
+    const uint32_t s0 = in ? v.start[w] : 0u;
+    vis[c] = a;
+    nb[c] = a & ~s0;
+    own[c] = nb[c] & owned_mask(w, v.lo, v.hi);
+    cnt += __popc(own[c]);
+    fr += __popc(nb[c]);
+  }
+  if (!kWrite) {
+    int64_t deg = 0;
+#pragma unroll
+    for (int c = 0; c < kChunks; ++c) {
+      unsigned m = __ballot_sync(0xffffffffu, own[c] != 0);
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t x = __shfl_sync(0xffffffffu, own[c], j);
+        if ((x >> lane) & 1u) {
+          const int64_t u = ((wbase + c * 32 + j) << 5) + lane;
+          deg += __ldg(off + u + 1) - __ldg(off + u);
+        }
+      }
     }
-    uint32_t mask = 0xFFFFFFFFu;
-    const int64_t vb = w << 5;
-    if (vb < v.lo) mask &= 0xFFFFFFFFu << (v.lo - vb);
-    if (vb + 32 > v.hi) mask &= (v.hi - vb) >= 32 ? 0xFFFFFFFFu : ((1u << (v.hi - vb)) - 1u);
-    own[j] = nb[j] & mask;
-    fr += __popc(nb[j]);
-    cnt += __popc(own[j]);
-    uint32_t x = own[j];
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      const int64_t u = vb + b;
-      deg += off[u + 1] - off[u];
+    cnt = block_sum_i64(cnt, red);
+    deg = block_sum_i64(deg, red);
+    fr = block_sum_i64(fr, red);
+    if (threadIdx.x == 0) {
+      v.block_sums[2 * bid] = cnt;
+      v.block_sums[2 * bid + 1] = deg;
+      if (fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+    }
+    return;
+  }
+  // write pass: per-warp prefix inside the block, block prefix from the scan
+  int64_t deg = 0;
+#pragma unroll
+  for (int c = 0; c < kChunks; ++c) {
+    unsigned m = __ballot_sync(0xffffffffu, own[c] != 0);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, own[c], j);
+      if ((x >> lane) & 1u) {
+        const int64_t u = ((wbase + c * 32 + j) << 5) + lane;
+        deg += __ldg(off + u + 1) - __ldg(off + u);
+      }
     }
   }
-  int64_t tot_cnt, tot_deg;
-  const int64_t ex_cnt = block_exclusive_i64(cnt, wsum, &tot_cnt);
-  const int64_t ex_deg = block_exclusive_i64(deg, wsum, &tot_deg);
+  cnt = warp_sum_i64(cnt);
+  deg = warp_sum_i64(deg);
+  if (lane == 0) {
+    s_wcnt[warp] = cnt;
+    s_wdeg[warp] = deg;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t c = lane < kWarps ? s_wcnt[lane] : 0, d = lane < kWarps ? s_wdeg[lane] : 0;
+    const int64_t ic = warp_inclusive_i64(c), id = warp_inclusive_i64(d);
+    if (lane < kWarps) {
+      s_wcnt[lane] = ic - c + v.block_sums[2 * bid];
+      s_wdeg[lane] = id - d + v.block_sums[2 * bid + 1];
+    }
+  }
+  __syncthreads();
+  int64_t pos = s_wcnt[warp];
+  int64_t epre = s_wdeg[warp];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int c = 0; c < kChunks; ++c) {
+    unsigned m = __ballot_sync(0xffffffffu, nb[c] != 0);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, nb[c], j);
+      const uint32_t xo = __shfl_sync(0xffffffffu, own[c], j);
+      const int64_t u = ((wbase + c * 32 + j) << 5) + lane;
+      if ((x >> lane) & 1u) v.level[u] = next_level;
+      if (xo) {
+        const bool has = (xo >> lane) & 1u;
+        int64_t r0 = 0, d = 0;
+        if (has) {
+          r0 = __ldg(off + u);
+          d = __ldg(off + u + 1) - r0;
+        }
+        const int64_t dinc = warp_inclusive_i64(d);
+        if (has) {
+          const int64_t p = pos + __popc(xo & lt);
+          const int64_t e = epre + dinc - d;
+          v.q_v[p] = (uint32_t)u;
+          v.q_pre[p] = e;
+          v.q_row[p] = r0;
+          for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d; ++t)
+            v.tile_vstart[t] = (uint32_t)p;
+        }
+        pos += __popc(xo);
+        epre += __shfl_sync(0xffffffffu, dinc, 31);
+      }
+    }
+    const int64_t w = wbase + c * 32 + lane;
+    if (nb[c] && w >= v.wlo && w < v.whi) v.start[w] = vis[c];
+  }
+}
+
+// Exclusive scan of the per-block (count, degree) pairs in place; totals
+// become the next level's q_local size and edge count.
+__global__ void __launch_bounds__(1024) k_commit_scan(PartView v, int64_t nblocks,
+                                                      RunCounters* run) {
+  __shared__ int64_t wsum[33];
+  __shared__ int64_t carry_c, carry_d;
+  if (threadIdx.x == 0) carry_c = carry_d = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nblocks; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t c = i < nblocks ? v.block_sums[2 * i] : 0;
+    const int64_t d = i < nblocks ? v.block_sums[2 * i + 1] : 0;
+    int64_t tc, td;
+    const int64_t ec = block_exclusive_i64(c, wsum, &tc);
+    const int64_t ed = block_exclusive_i64(d, wsum, &td);
+    const int64_t cc = carry_c, cd = carry_d;
+    if (i < nblocks) {
+      v.block_sums[2 * i] = cc + ec;
+      v.block_sums[2 * i + 1] = cd + ed;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry_c = cc + tc;
+      carry_d = cd + td;
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    int64_t pc = 0, pd = 0;
-    if (bid == 0) {
-      lb_publish(v.scan_state, 0, 2, tot_cnt, tot_deg);
-    } else {
-      lb_publish(v.scan_state, bid, 1, tot_cnt, tot_deg);
-      int64_t j = bid - 1;
-      while (true) {
-        volatile uint64_t* s = v.scan_state + 3 * j;
-        uint64_t f;
-        do { f = s[0]; } while (f == 0);
-        __threadfence();
-        pc += (int64_t)s[1];
-        pd += (int64_t)s[2];
-        if (f == 2) break;
-        --j;
-      }
-      lb_publish(v.scan_state, bid, 2, pc + tot_cnt, pd + tot_deg);
-    }
-    s_excl_cnt = pc;
-    s_excl_deg = pd;
-    if (bid == nblocks - 1) {
-      v.ctr->q_count = pc + tot_cnt;
-      v.ctr->q_edges = pd + tot_deg;
-      atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)(pd + tot_deg));
-    }
+    v.ctr->q_count = carry_c;
+    v.ctr->q_edges = carry_d;
+    atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)carry_d);
   }
-  __syncthreads();
-  int64_t pos = s_excl_cnt + ex_cnt;
-  int64_t epre = s_excl_deg + ex_deg;
-#pragma unroll
-  for (int j = 0; j < kCommitWords; ++j) {
-    const int64_t w = w0 + j;
-    if (w < v.wlo || w >= v.whi) continue;
-    const int64_t vb = w << 5;
-    uint32_t x = nb[j];
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      const int64_t u = vb + b;
-      v.level[u] = next_level;
-      if ((own[j] >> b) & 1u) {
-        const int64_t r0 = off[u], d = off[u + 1] - r0;
-        v.q_v[pos] = (uint32_t)u;
-        v.q_pre[pos] = epre;
-        v.q_row[pos] = r0;
-        for (int64_t t = (epre + kTile - 1) / kTile; t * kTile < epre + d; ++t)
-          v.tile_vstart[t] = (uint32_t)pos;
-        ++pos;
-        epre += d;
-      }
-    }
-    v.start[w] = vis[j];
-  }
-  fr = block_sum_i64(fr, red);
-  if (threadIdx.x == 0 && fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
 }
 
 __global__ void k_commit_rest(PartView v, uint32_t next_level) {
@@ -464,12 +560,9 @@ unsigned grid_cap(int64_t work, int block, int num_sms, int per_sm = 8) {
 struct EngineTables {
   DevBuf<uint32_t*> pubs, visiteds, parents;
   DevBuf<PartCounters*> ctrs;
-  DevBuf<uint64_t*> scan_states;
-  DevBuf<int64_t> scan_words;
   std::vector<DevBuf<int32_t>> round_tables;
   std::vector<RoundDesc> rounds;
   DevBuf<uint32_t> parents_final;  // assembled output parents when num_parts > 1
-  int64_t scan_words_max = 0;
   cudaEvent_t ev[6] = {};
   ~EngineTables() {
     for (auto& e : ev)
@@ -526,8 +619,6 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
   ctx->parts.resize(parts);
   std::vector<uint32_t*> pubs(parts), viss(parts), pars(parts);
   std::vector<PartCounters*> ctrs(parts);
-  std::vector<uint64_t*> sstates(parts);
-  std::vector<int64_t> swords(parts);
   for (int g = 0; g < parts; ++g) {
     Part& p = ctx->parts[g];
     p.lo = bounds[g];
@@ -547,10 +638,8 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_TRY(p.q_pre.alloc(owned + 1));
     BFB_TRY(p.q_row.alloc(owned + 1));
     BFB_TRY(p.tile_vstart.alloc(p.tile_cap));
-    const int64_t cblocks =
-        (p.whi - (p.wlo & ~(int64_t)(kCommitWords - 1)) + kWordsPerCommitBlock - 1) /
-            kWordsPerCommitBlock + 1;
-    BFB_TRY(p.scan_state.alloc(3 * cblocks));
+    const int64_t cblocks = commit_blocks(p.wlo, p.whi) + 1;
+    BFB_TRY(p.block_sums.alloc(2 * cblocks));
     BFB_TRY(p.ctr.alloc(1));
     BFB_CUDA(cudaMemset(p.visited.p, 0, nwords_pad * sizeof(uint32_t)));
     BFB_CUDA(cudaMemset(p.start.p, 0, nwords_pad * sizeof(uint32_t)));
@@ -560,24 +649,15 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     viss[g] = p.visited.p;
     pars[g] = p.parent.p;
     ctrs[g] = p.ctr.p;
-    sstates[g] = p.scan_state.p;
-    swords[g] = 3 * cblocks;
-    D->scan_words_max = std::max(D->scan_words_max, 3 * cblocks);
   }
   BFB_TRY(D->pubs.alloc(parts));
   BFB_TRY(D->visiteds.alloc(parts));
   BFB_TRY(D->parents.alloc(parts));
   BFB_TRY(D->ctrs.alloc(parts));
-  BFB_TRY(D->scan_states.alloc(parts));
-  BFB_TRY(D->scan_words.alloc(parts));
   BFB_CUDA(cudaMemcpy(D->pubs.p, pubs.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
   BFB_CUDA(cudaMemcpy(D->visiteds.p, viss.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
   BFB_CUDA(cudaMemcpy(D->parents.p, pars.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
   BFB_CUDA(cudaMemcpy(D->ctrs.p, ctrs.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
-  BFB_CUDA(cudaMemcpy(D->scan_states.p, sstates.data(), parts * sizeof(void*),
-                      cudaMemcpyHostToDevice));
-  BFB_CUDA(cudaMemcpy(D->scan_words.p, swords.data(), parts * sizeof(int64_t),
-                      cudaMemcpyHostToDevice));
   // round tables
   for (auto& rnd : ctx->schedule) {
     std::vector<int32_t> dst, src, first(parts + 1, 0);
@@ -616,6 +696,14 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<true>, kExpandBlock, 0));
   else
     BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<false>, kExpandBlock, 0));
+  // Developer knobs for tuning runs: cap resident expand blocks per SM and
+  // the shared-memory carveout (percent); unset = occupancy maximum.
+  if (const char* e = std::getenv("BFB_EXPAND_OCC")) occ = std::min(occ, std::max(1, std::atoi(e)));
+  if (const char* e = std::getenv("BFB_CARVEOUT")) {
+    const int pct = std::atoi(e);
+    BFB_CUDA(cudaFuncSetAttribute(k_expand<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    BFB_CUDA(cudaFuncSetAttribute(k_expand<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  }
   ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
   for (auto& ev : D->ev) BFB_CUDA(cudaEventCreate(&ev));
   ctx->engine_ready = true;
@@ -700,18 +788,18 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[4], s));
     // Commit: levels, start snapshot, next q_local, frontier count.
-    k_commit_prep<<<grid_cap(D->scan_words_max, 256, sms, 1), 256, 0, s>>>(
-        D->ctrs.p, P, D->scan_states.p, D->scan_words.p);
+    k_commit_prep<<<1, 256, 0, s>>>(D->ctrs.p, P);
     ++launches;
     const uint32_t next_level = (uint32_t)(level + 1);
     for (int g = 0; g < P; ++g) {
       Part& p = ctx->parts[g];
       PartView v = view_of(ctx, p);
       if (p.whi > p.wlo) {
-        const int64_t cb = (p.whi - (p.wlo & ~(int64_t)(kCommitWords - 1)) +
-                            kWordsPerCommitBlock - 1) / kWordsPerCommitBlock;
-        k_commit_owned<<<(unsigned)cb, kCommitBlock, 0, s>>>(v, off, next_level, ctx->run.p);
-        ++launches;
+        const int64_t cb = commit_blocks(p.wlo, p.whi);
+        k_commit_owned<false><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, off, next_level);
+        k_commit_scan<<<1, 1024, 0, s>>>(v, cb, ctx->run.p);
+        k_commit_owned<true><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, off, next_level);
+        launches += 3;
       }
       if (nwords - (p.whi - p.wlo) > 0) {
         k_commit_rest<<<small_grid, 256, 0, s>>>(v, next_level);

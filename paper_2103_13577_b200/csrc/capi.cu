@@ -164,6 +164,8 @@ void bfb_destroy(bfb_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   engine_release(ctx);
   ctx->g = DevGraph();
+  for (auto& e : ctx->timer)
+    if (e) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -171,6 +173,27 @@ void bfb_destroy(bfb_ctx* ctx) {
 int bfb_set_timing(bfb_ctx* ctx, int enabled) {
   CTX_GUARD(ctx);
   ctx->timing = enabled != 0;
+  return BFB_OK;
+}
+
+int bfb_timer_start(bfb_ctx* ctx) {
+  CTX_GUARD(ctx);
+  if (!ctx->timer[0]) {
+    BFB_CUDA(cudaEventCreate(&ctx->timer[0]));
+    BFB_CUDA(cudaEventCreate(&ctx->timer[1]));
+  }
+  BFB_CUDA(cudaEventRecord(ctx->timer[0], ctx->stream));
+  return BFB_OK;
+}
+
+int bfb_timer_stop(bfb_ctx* ctx, double* elapsed_ms_out) {
+  CTX_GUARD(ctx);
+  if (!ctx->timer[0]) return fail(BFB_ERR_STATE, "timer not started");
+  BFB_CUDA(cudaEventRecord(ctx->timer[1], ctx->stream));
+  BFB_CUDA(cudaEventSynchronize(ctx->timer[1]));
+  float ms = 0;
+  BFB_CUDA(cudaEventElapsedTime(&ms, ctx->timer[0], ctx->timer[1]));
+  if (elapsed_ms_out) *elapsed_ms_out = ms;
   return BFB_OK;
 }
 

@@ -155,6 +155,14 @@ class DeviceGraph:
     def num_parts(self):
         return len(self._engine_key[0]) - 1 if self._engine_key else 0
 
+    def timer_start(self):
+        check(_lib.load().bfb_timer_start(self.handle))
+
+    def timer_stop(self):
+        ms = ctypes.c_double()
+        check(_lib.load().bfb_timer_stop(self.handle, byref(ms)))
+        return ms.value
+
     def set_timing(self, enabled):
         check(_lib.load().bfb_set_timing(self.handle, 1 if enabled else 0))
 

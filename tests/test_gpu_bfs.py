@@ -1,0 +1,196 @@
+"""engine.run on B200 vs the oracle: levels bit-exact, RunStats identical to
+the lockstep oracle engine, parents valid; SPEC.md acceptance criteria 1,3,4,
+7,8 through the C ABI; full-size properties at scale 24."""
+
+import numpy as np
+import pytest
+
+from oracle import bfs as ob
+from oracle import engine as oe
+from oracle import schedule as osch
+from oracle import validate as ov
+from paper_2103_13577_b200 import engine, graphs
+from tests import util
+from tests.util import sha16
+
+pytestmark = pytest.mark.gpu
+U = 0xFFFFFFFF
+
+
+def _g(off, adj):
+    return graphs.Graph(off.size - 1, adj.size, off.copy(), adj.copy())
+
+
+def _same_stats(st, ost):
+    return (st.per_level_frontier_size == ost.per_level_frontier_size
+            and st.levels == ost.levels
+            and st.remote_messages == ost.remote_messages
+            and st.remote_vertices_transferred == ost.remote_vertices_transferred
+            and st.rounds_executed == ost.rounds_executed
+            and st.buffer_high_water == ost.buffer_high_water
+            and st.traversed_edges == ost.traversed_edges)
+
+
+def test_spec_examples():
+    off, adj = util.path_graph(3)
+    g = _g(off, adj)
+    d, st = engine.run(g, graphs.partition_1d(g, 1), 0)
+    assert d.d.tolist() == [0, 1, 2] and d.root == 0
+    off, adj = util.csr_of_undirected(4, [(0, 1), (2, 3)])
+    g = _g(off, adj)
+    assert engine.run(g, graphs.partition_1d(g, 1), 0)[0].d.tolist() == [0, 1, U, U]
+    off, adj = util.star_graph(5)
+    g = _g(off, adj)
+    assert engine.run(g, graphs.partition_1d(g, 1), 0)[1].per_level_frontier_size == [1, 5]
+    off, adj = util.path_graph(5)
+    g = _g(off, adj)
+    d, st = engine.run(g, graphs.partition_1d(g, 2), 0, engine.EngineConfig(fanout=1))
+    assert d.d.tolist() == [0, 1, 2, 3, 4] and st.levels == 5
+
+
+def test_errors():
+    off, adj = util.path_graph(6)
+    g = _g(off, adj)
+    p = graphs.partition_1d(g, 2)
+    with pytest.raises(ValueError):
+        engine.run(g, p, 6)
+    with pytest.raises(ValueError):
+        engine.run(g, p, -1)
+    with pytest.raises(ValueError):
+        engine.run(g, p, 0, engine.EngineConfig(fanout=3))
+    with pytest.raises(ValueError):
+        engine.run(g, graphs.Partition(2, [0, 3, 5]), 0)
+    with pytest.raises(ValueError):
+        engine.EngineConfig(strategy="ring")
+
+
+def test_golden_levels_s16(golden):
+    e = golden["s16_ef8"]
+    g = graphs.kronecker(16, 8, 1)
+    p = graphs.partition_1d(g, 1)
+    for r, want in e["bfs"].items():
+        d, st = engine.run(g, p, int(r), engine.EngineConfig(parents=True))
+        assert sha16(d.d) == want["levels_sha"], r
+        assert st.per_level_frontier_size == want["sizes"]
+        assert st.traversed_edges == want["traversed_edges"]
+        assert g.device.validate(int(r)) == 0
+        assert not ov.check_parents(g.offsets, g.adjacency, int(r), d.d, d.parents)
+
+
+def test_golden_levels_s20(golden):
+    e = golden["s20_ef8"]
+    g = graphs.kronecker(20, 8, 1)
+    for P, f in ((1, 1), (4, 2), (8, 8)):
+        p = graphs.partition_1d(g, P)
+        for r, want in list(e["bfs"].items())[:4]:
+            d, st = engine.run(g, p, int(r), engine.EngineConfig(fanout=f))
+            assert sha16(d.d) == want["levels_sha"], (P, f, r)
+            assert st.per_level_frontier_size == want["sizes"]
+
+
+def _sweep_graphs():
+    yield "rmat13", util.rmat_graph(13)
+    yield "gnp", util.gnp_graph(5000, 0.002)
+    yield "path", util.path_graph(10000)
+    yield "star", util.star_graph(300)
+    yield "components", util.components_graph()
+
+
+@pytest.mark.parametrize("cn", [1, 2, 3, 4, 7, 8, 9, 12, 16])
+def test_acceptance_sweep_vs_oracle_engine(cn):
+    """Acceptance 1,3,4,7,8 at reduced root counts: levels
+    equal bfs_top_down, RunStats equal the lockstep oracle engine's for both
+    strategies, buffer high-water within f*|V|, rounds = levels*num_rounds."""
+    rng = np.random.default_rng(100 + cn)
+    for name, (off, adj) in _sweep_graphs():
+        n = off.size - 1
+        g = _g(off, adj)
+        p = graphs.partition_1d(g, cn)
+        roots = rng.choice(n, 3, replace=False)
+        for f in sorted({1, min(2, cn), min(4, cn), cn}):
+            for r in roots:
+                r = int(r)
+                ref = ob.bfs_top_down(off, adj, r)
+                for strat in ("butterfly", "all2all"):
+                    d, st = engine.run(g, p, r, engine.EngineConfig(fanout=f, strategy=strat,
+                                                                  parents=True))
+                    assert np.array_equal(d.d, ref), (name, cn, f, r, strat)
+                    _, ost = oe.run(off, adj, p.boundaries, r, fanout=f, strategy=strat)
+                    assert _same_stats(st, ost), (name, cn, f, r, strat, st, ost)
+                    assert max(st.buffer_high_water) <= f * n or strat == "all2all"
+                    if strat == "butterfly":
+                        assert st.rounds_executed == st.levels * osch.num_rounds(cn, f)
+                    assert not ov.check_parents(off, adj, r, d.d, d.parents)
+
+
+def test_all2all_message_reduction_cn16():
+    off, adj = util.gnp_graph(3000, 0.01)
+    g = _g(off, adj)
+    p = graphs.partition_1d(g, 16)
+    da, sa = engine.run(g, p, 0, engine.EngineConfig(strategy="all2all"))
+    d1, s1 = engine.run(g, p, 0, engine.EngineConfig(fanout=1))
+    d4, s4 = engine.run(g, p, 0, engine.EngineConfig(fanout=4))
+    assert np.array_equal(da.d, d1.d) and np.array_equal(da.d, d4.d)
+    assert sa.remote_messages >= 240 > 0
+    assert s1.remote_messages <= 64 * s1.levels and s4.remote_messages <= 96 * s4.levels
+
+
+def test_isolated_root_and_determinism():
+    g = graphs.kronecker(14, 8, 1)
+    off = g.offsets
+    iso = int(np.flatnonzero(np.diff(off) == 0)[0])
+    p = graphs.partition_1d(g, 4)
+    d, st = engine.run(g, p, iso, engine.EngineConfig(fanout=2))
+    assert st.per_level_frontier_size == [1] and (d.d != U).sum() == 1
+    a, _ = engine.run(g, p, 3, engine.EngineConfig(fanout=2))
+    b, _ = engine.run(g, p, 3, engine.EngineConfig(fanout=2))
+    assert np.array_equal(a.d, b.d)
+
+
+def test_reference_graph_objects(reference_graphs):
+    R = reference_graphs
+    rg = R.build_csr(R.symmetrize(R.generate_rmat(12, 8, 3)))
+    rp = R.partition_1d(rg, 3)
+    d, st = engine.run(rg, rp, 5, engine.EngineConfig(fanout=2))
+    assert np.array_equal(d.d, ob.bfs_top_down(rg.offsets, rg.adjacency, 5))
+
+
+@pytest.mark.slow
+def test_scale24_full_size_properties():
+    """Full-size (s24 ef16) checks without a CPU BFS: device certificate
+    (SPEC.md:130-132 + parent validity), run-to-run determinism, CN=1 vs CN=4
+    agreement, and frontier sizes summing to the reached count."""
+    g = graphs.kronecker(24, 16, 1)
+    dg = g.device
+    roots = graphs.sample_roots(g, 3)
+    dg.setup(dg.partition_1d(1), 1, "butterfly", parents=True)
+    ref = {}
+    for r in roots:
+        lv, _, sizes, st, _ = dg.bfs(int(r))
+        assert dg.validate(int(r)) == 0
+        assert sum(sizes) == st.reached == int((lv != U).sum())
+        ref[int(r)] = sha16(lv)
+        lv2, _, _, _, _ = dg.bfs(int(r))
+        assert sha16(lv2) == ref[int(r)]
+    dg.setup(dg.partition_1d(4), 2, "butterfly", parents=True)
+    for r in roots:
+        lv, _, _, _, _ = dg.bfs(int(r))
+        assert sha16(lv) == ref[int(r)]
+        assert dg.validate(int(r)) == 0
+
+
+@pytest.mark.slow
+def test_scale24_golden(golden):
+    e = golden.get("s24_ef16")
+    if e is None:
+        pytest.skip("s24 golden not generated")
+    g = graphs.kronecker(24, 16, 1)
+    assert g.num_edges == e["num_edges"]
+    dg = g.device
+    off, adj = dg.csr()
+    assert sha16(off) == e["offsets_sha"] and sha16(adj) == e["adjacency_sha"]
+    assert dg.partition_1d(8).tolist() == e["partitions"]["8"]
+    dg.setup(dg.partition_1d(1), 1, "butterfly")
+    for r, want in e["bfs"].items():
+        lv, _, sizes, st, _ = dg.bfs(int(r))
+        assert sha16(lv) == want["levels_sha"] and sizes == want["sizes"]

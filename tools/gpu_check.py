@@ -119,6 +119,24 @@ if __name__ == "__main__":
             stage("small", small)
         elif w == "mid":
             stage("mid", mid)
+        elif w.startswith("prof"):
+            # prof<scale>: one parents=True BFS (profiling target)
+            sc = int(w[4:6])
+            from paper_2103_13577_b200 import graphs as _g
+
+            gg = _g.kronecker(sc, 16 if sc in (24, 27) else 8, 1)
+            gg.device.setup(gg.device.partition_1d(1), 1, "butterfly", parents=True)
+            r = int(_g.sample_roots(gg, 1)[0])
+            _, _, sz, st, _ = gg.device.bfs(r, levels=False)
+            print("prof bfs", r, sz, st.elapsed_ms, flush=True)
+        elif w.startswith("occ"):
+            # occ<scale>: sweep expand blocks/SM (env knob read at setup)
+            sc = int(w[3:5])
+            for occ in ("2", "3", "4", "6", "8"):
+                os.environ["BFB_EXPAND_OCC"] = occ
+                print("BFB_EXPAND_OCC", occ, flush=True)
+                stage(w + "/" + occ, big(sc, 16 if sc in (24, 27) else 8, nroots=3))
+            os.environ.pop("BFB_EXPAND_OCC")
         elif w.startswith("s"):
             sc = int(w[1:3])
             ef = 16 if sc in (24, 27) else 8
