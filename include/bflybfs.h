@@ -65,6 +65,10 @@ const char* bfb_version(void);
 const char* bfb_last_error(void);
 int bfb_device_count(int* count_out);
 
+/* Page-locked host memory for result arrays (fast D2H of levels/parents). */
+int bfb_host_alloc(size_t bytes, void** ptr_out);
+void bfb_host_free(void* ptr);
+
 /* ---- butterfly-schedule (host-only, no GPU needed) ------ */
 /* num_rounds(CN, f): SPEC.md:202-210 */
 int bfb_num_rounds(int num_nodes, int fanout, int* rounds_out);
@@ -135,6 +139,9 @@ int bfb_engine_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int
 int bfb_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_out,
             int64_t* frontier_sizes_out, int64_t max_levels, int64_t* buffer_high_water_out,
             bfb_run_stats* stats_out);
+/* per_level_frontier_size of the last run (all levels; bfb_bfs's array may be
+ * capped by max_levels): writes min(cap, levels) entries, *len_out = levels. */
+int bfb_frontier_sizes(bfb_ctx* ctx, int64_t* out, int64_t cap, int64_t* len_out);
 /* D2H of the last run's results (node 0's view). */
 int bfb_copy_levels(bfb_ctx* ctx, uint32_t* levels_out);
 int bfb_copy_parents(bfb_ctx* ctx, int64_t* parents_out);
@@ -142,6 +149,35 @@ int bfb_copy_parents(bfb_ctx* ctx, int64_t* parents_out);
  * parents: *errors_out = bitmask (1 root, 2 reachability mismatch on an edge,
  * 4 edge spans >1 level, 8 reached vertex without predecessor, 16 bad parent). */
 int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out);
+
+/* ---- multi-process mode: one process per GPU (torchrun), node = rank -----
+ * The host driver (paper_2103_13577_b200/dist.py) sequences one level as
+ * expand -> for each butterfly round: publish, [barrier + snapshot-size
+ * allgather], merge -> commit.  Peers' round snapshots are read in place from
+ * their HBM through CUDA IPC mappings (NVLink peer loads), fused with the OR
+ * merge; the reference's CopyFrontier(Q_global[srcCN]) without
+ * a staging copy. */
+/* init's allocation step for node `rank` only (global partition boundaries). */
+int bfb_rank_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int fanout,
+                   int strategy, int want_parents, int rank);
+/* 128 bytes: the IPC handles of this node's two (round-parity) snapshot buffers. */
+int bfb_rank_ipc_handles(bfb_ctx* ctx, void* handles_out);
+int bfb_rank_open_peer(bfb_ctx* ctx, int peer, const void* handles);
+int bfb_rank_begin(bfb_ctx* ctx, int64_t root);
+int bfb_rank_expand(bfb_ctx* ctx);
+/* Snapshot this node's q_global_next (round start); returns its size. */
+int bfb_rank_publish(bfb_ctx* ctx, int parity, int64_t* count_out);
+/* Merge the given sources' snapshots (sizes from the allgather; empty skipped). */
+int bfb_rank_merge(bfb_ctx* ctx, int parity, const int32_t* sources, const int64_t* counts,
+                   int num_sources);
+/* Commit the level; returns the synchronized frontier size (0 = terminate)
+ * and this node's owned share of it (|q_local|; sums to the frontier). */
+int bfb_rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out);
+/* End of run: device elapsed time and this node's counters. */
+int bfb_rank_finish(bfb_ctx* ctx, bfb_run_stats* stats_out);
+/* This node's phase-1 parents (uint32, 0xFFFFFFFF = none): min over nodes is
+ * a valid parent array. */
+int bfb_rank_parents_raw(bfb_ctx* ctx, uint32_t* parents_out);
 
 #ifdef __cplusplus
 }

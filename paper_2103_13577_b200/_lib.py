@@ -54,6 +54,8 @@ _SIGNATURES = {
     "bfb_version": (c_char_p, []),
     "bfb_last_error": (c_char_p, []),
     "bfb_device_count": (c_int, [POINTER(c_int)]),
+    "bfb_host_alloc": (c_int, [ctypes.c_size_t, POINTER(c_void_p)]),
+    "bfb_host_free": (None, [c_void_p]),
     "bfb_num_rounds": (c_int, [c_int, c_int, POINTER(c_int)]),
     "bfb_make_schedule": (c_int, [c_int, c_int, c_int, _I32P, c_int64, _I64P]),
     "bfb_message_count_paper": (c_int, [c_int, c_int, _I64P]),
@@ -76,9 +78,20 @@ _SIGNATURES = {
     "bfb_engine_setup": (c_int, [c_void_p, c_int, _I64P, c_int, c_int, c_int]),
     "bfb_bfs": (c_int, [c_void_p, c_int64, _U32P, _I64P, _I64P, c_int64, _I64P,
                         POINTER(RunStatsC)]),
+    "bfb_frontier_sizes": (c_int, [c_void_p, _I64P, c_int64, _I64P]),
     "bfb_copy_levels": (c_int, [c_void_p, _U32P]),
     "bfb_copy_parents": (c_int, [c_void_p, _I64P]),
     "bfb_validate": (c_int, [c_void_p, c_int64, _I64P]),
+    "bfb_rank_setup": (c_int, [c_void_p, c_int, _I64P, c_int, c_int, c_int, c_int]),
+    "bfb_rank_ipc_handles": (c_int, [c_void_p, c_void_p]),
+    "bfb_rank_open_peer": (c_int, [c_void_p, c_int, c_void_p]),
+    "bfb_rank_begin": (c_int, [c_void_p, c_int64]),
+    "bfb_rank_expand": (c_int, [c_void_p]),
+    "bfb_rank_publish": (c_int, [c_void_p, c_int, _I64P]),
+    "bfb_rank_merge": (c_int, [c_void_p, c_int, _I32P, _I64P, c_int]),
+    "bfb_rank_commit": (c_int, [c_void_p, _I64P, _I64P]),
+    "bfb_rank_finish": (c_int, [c_void_p, POINTER(RunStatsC)]),
+    "bfb_rank_parents_raw": (c_int, [c_void_p, _U32P]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -169,6 +169,7 @@ struct Part {
   DevBuf<uint32_t> level;          // d_local (n)
   DevBuf<uint32_t> parent;         // phase-1 parents (n) when wanted
   DevBuf<uint32_t> pub;            // published round snapshot (n bits)
+  DevBuf<uint32_t> pub_alt;        // odd-round snapshot (multi-process mode)
   DevBuf<uint32_t> q_v;            // q_local vertex ids, ascending
   DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local
   DevBuf<int64_t> q_row;           // offsets[v] of each q_local vertex
@@ -204,6 +205,7 @@ struct bfb_ctx {
   bool have_run = false;
   int64_t last_root = -1;
   int64_t last_levels = 0;
+  std::vector<int64_t> last_sizes;     // per_level_frontier_size of the last run
   int64_t launches = 0;
   cudaEvent_t timer[2] = {nullptr, nullptr};
 };
@@ -240,6 +242,19 @@ int engine_copy_levels(bfb_ctx* ctx, uint32_t* out);
 int engine_copy_parents(bfb_ctx* ctx, int64_t* out);
 int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs);
 void engine_release(bfb_ctx* ctx);
+
+// bfs_engine.cu, multi-process mode: this context is node `rank` of CN
+int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int strategy,
+               int want_parents, int rank);
+int rank_ipc_handles(bfb_ctx* ctx, void* out);
+int rank_open_peer(bfb_ctx* ctx, int peer, const void* handles);
+int rank_begin(bfb_ctx* ctx, int64_t root);
+int rank_expand(bfb_ctx* ctx);
+int rank_publish(bfb_ctx* ctx, int parity, int64_t* count_out);
+int rank_merge(bfb_ctx* ctx, int parity, const int32_t* srcs, const int64_t* counts, int nsrc);
+int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out);
+int rank_finish(bfb_ctx* ctx, bfb_run_stats* st);
+int rank_parents_raw(bfb_ctx* ctx, uint32_t* out);
 
 // schedule (capi.cu)
 int make_schedule(int cn, int fanout, int strategy, std::vector<std::vector<std::vector<int>>>& out);

@@ -303,6 +303,33 @@ __device__ __forceinline__ uint32_t owned_mask(int64_t w, int64_t lo, int64_t hi
   return mask;
 }
 
+// Sum of degrees of the owned new vertices held in own[] (lane = bit), with
+// kCommitBatch words' offsets loads in flight per iteration.
+constexpr int kCommitBatch = 8;
+
+template <int kChunks>
+__device__ __forceinline__ int64_t commit_degree_sum(const uint32_t (&own)[kChunks], int64_t wbase,
+                                                     int lane, const int64_t* __restrict__ off) {
+  int64_t deg = 0;
+#pragma unroll
+  for (int c = 0; c < kChunks; ++c) {
+    const unsigned m = __ballot_sync(0xffffffffu, own[c] != 0);
+#pragma unroll 1
+    for (int g8 = 0; g8 < 32; g8 += kCommitBatch) {
+      if (!((m >> g8) & ((1u << kCommitBatch) - 1u))) continue;
+#pragma unroll
+      for (int k = 0; k < kCommitBatch; ++k) {
+        const uint32_t x = __shfl_sync(0xffffffffu, own[c], g8 + k);
+        if ((x >> lane) & 1u) {
+          const int64_t u = ((wbase + c * 32 + g8 + k) << 5) + lane;
+          deg += __ldg(off + u + 1) - __ldg(off + u);
+        }
+      }
+    }
+  }
+  return deg;
+}
+
 // Commit of the owned words, as reduce (kWrite = false) -> scan -> write
 // (kWrite = true) over 1024-word blocks.  Lane l of a warp holds word
 // (chunk base + l) of each chunk; vertex work then runs with lane = bit, so
@@ -336,20 +363,7 @@ __global__ void __launch_bounds__(kCommitBlock) k_commit_owned(PartView v,
     fr += __popc(nb[c]);
   }
   if (!kWrite) {
-    int64_t deg = 0;
-#pragma unroll
-    for (int c = 0; c < kChunks; ++c) {
-      unsigned m = __ballot_sync(0xffffffffu, own[c] != 0);
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t x = __shfl_sync(0xffffffffu, own[c], j);
-        if ((x >> lane) & 1u) {
-          const int64_t u = ((wbase + c * 32 + j) << 5) + lane;
-          deg += __ldg(off + u + 1) - __ldg(off + u);
-        }
-      }
-    }
+    int64_t deg = commit_degree_sum<kChunks>(own, wbase, lane, off);
     cnt = block_sum_i64(cnt, red);
     deg = block_sum_i64(deg, red);
     fr = block_sum_i64(fr, red);
@@ -361,20 +375,7 @@ __global__ void __launch_bounds__(kCommitBlock) k_commit_owned(PartView v,
     return;
   }
   // write pass: per-warp prefix inside the block, block prefix from the scan
-  int64_t deg = 0;
-#pragma unroll
-  for (int c = 0; c < kChunks; ++c) {
-    unsigned m = __ballot_sync(0xffffffffu, own[c] != 0);
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      const uint32_t x = __shfl_sync(0xffffffffu, own[c], j);
-      if ((x >> lane) & 1u) {
-        const int64_t u = ((wbase + c * 32 + j) << 5) + lane;
-        deg += __ldg(off + u + 1) - __ldg(off + u);
-      }
-    }
-  }
+  int64_t deg = commit_degree_sum<kChunks>(own, wbase, lane, off);
   cnt = warp_sum_i64(cnt);
   deg = warp_sum_i64(deg);
   if (lane == 0) {
@@ -396,33 +397,43 @@ __global__ void __launch_bounds__(kCommitBlock) k_commit_owned(PartView v,
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int c = 0; c < kChunks; ++c) {
-    unsigned m = __ballot_sync(0xffffffffu, nb[c] != 0);
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      const uint32_t x = __shfl_sync(0xffffffffu, nb[c], j);
-      const uint32_t xo = __shfl_sync(0xffffffffu, own[c], j);
-      const int64_t u = ((wbase + c * 32 + j) << 5) + lane;
-      if ((x >> lane) & 1u) v.level[u] = next_level;
-      if (xo) {
-        const bool has = (xo >> lane) & 1u;
-        int64_t r0 = 0, d = 0;
-        if (has) {
-          r0 = __ldg(off + u);
-          d = __ldg(off + u + 1) - r0;
+    const unsigned m = __ballot_sync(0xffffffffu, nb[c] != 0);
+#pragma unroll 1
+    for (int g8 = 0; g8 < 32; g8 += kCommitBatch) {
+      if (!((m >> g8) & ((1u << kCommitBatch) - 1u))) continue;
+      uint32_t x[kCommitBatch], xo[kCommitBatch];
+      int64_t r0[kCommitBatch], d[kCommitBatch];
+#pragma unroll
+      for (int k = 0; k < kCommitBatch; ++k) {  // batch the offsets loads (MLP)
+        x[k] = __shfl_sync(0xffffffffu, nb[c], g8 + k);
+        xo[k] = __shfl_sync(0xffffffffu, own[c], g8 + k);
+        const int64_t u = ((wbase + c * 32 + g8 + k) << 5) + lane;
+        r0[k] = 0;
+        d[k] = 0;
+        if ((xo[k] >> lane) & 1u) {
+          r0[k] = __ldg(off + u);
+          d[k] = __ldg(off + u + 1) - r0[k];
         }
-        const int64_t dinc = warp_inclusive_i64(d);
-        if (has) {
-          const int64_t p = pos + __popc(xo & lt);
-          const int64_t e = epre + dinc - d;
-          v.q_v[p] = (uint32_t)u;
-          v.q_pre[p] = e;
-          v.q_row[p] = r0;
-          for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d; ++t)
-            v.tile_vstart[t] = (uint32_t)p;
+      }
+#pragma unroll
+      for (int k = 0; k < kCommitBatch; ++k) {
+        const int64_t u = ((wbase + c * 32 + g8 + k) << 5) + lane;
+        if ((x[k] >> lane) & 1u) v.level[u] = next_level;
+        if (xo[k]) {
+          const bool has = (xo[k] >> lane) & 1u;
+          const int64_t dinc = warp_inclusive_i64(d[k]);
+          if (has) {
+            const int64_t p = pos + __popc(xo[k] & lt);
+            const int64_t e = epre + dinc - d[k];
+            v.q_v[p] = (uint32_t)u;
+            v.q_pre[p] = e;
+            v.q_row[p] = r0[k];
+            for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d[k]; ++t)
+              v.tile_vstart[t] = (uint32_t)p;
+          }
+          pos += __popc(xo[k]);
+          epre += __shfl_sync(0xffffffffu, dinc, 31);
         }
-        pos += __popc(xo);
-        epre += __shfl_sync(0xffffffffu, dinc, 31);
       }
     }
     const int64_t w = wbase + c * 32 + lane;
@@ -553,6 +564,27 @@ unsigned grid_cap(int64_t work, int block, int num_sms, int per_sm = 8) {
   return (unsigned)g;
 }
 
+// Multi-process merge: OR the round's source snapshots (peer memory mapped
+// over NVLink by CUDA IPC, or local) into this node's visited bitmap.  This
+// node is the only writer of its bitmap during the merge, so no atomics.
+constexpr int kMaxSrc = 64;
+struct SrcList {
+  const uint32_t* p[kMaxSrc];
+  int n;
+};
+
+__global__ void k_merge_peers(SrcList L, uint32_t* __restrict__ vis, int64_t nwords) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    for (int i = 0; i < L.n; ++i) acc |= L.p[i][w];
+    if (acc) {
+      const uint32_t cur = vis[w];
+      if (acc & ~cur) vis[w] = cur | acc;
+    }
+  }
+}
+
 }  // namespace
 
 // Device-side tables built at setup (pointer arrays indexed by node, the
@@ -564,7 +596,14 @@ struct EngineTables {
   std::vector<RoundDesc> rounds;
   DevBuf<uint32_t> parents_final;  // assembled output parents when num_parts > 1
   cudaEvent_t ev[6] = {};
+  // multi-process mode (rank >= 0): this context holds node `rank` only
+  int rank = -1;
+  std::vector<const uint32_t*> peer_pub[2];  // per node, by round parity
+  std::vector<void*> opened;                 // IPC mappings to close
+  int64_t level = 0, reached = 0, launches = 0, levels = 0;
+  int64_t remote_messages = 0, remote_vertices = 0, high_water = 0, exchange_bytes = 0;
   ~EngineTables() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
   }
@@ -748,6 +787,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   int64_t nsizes = 0;
   if (max_levels > 0 && sizes_out) sizes_out[0] = 1;
   nsizes = 1;
+  ctx->last_sizes.assign(1, 1);
   int64_t reached = 1;
   const unsigned small_grid = grid_cap(nwords, 256, sms, 4);
   while (true) {
@@ -824,6 +864,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     const int64_t frontier = ctx->pinned[0];
     if (frontier == 0) break;
     if (nsizes < max_levels && sizes_out) sizes_out[nsizes] = frontier;
+    ctx->last_sizes.push_back(frontier);
     ++nsizes;
     reached += frontier;
     ++level;
@@ -921,6 +962,233 @@ int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs) {
   BFB_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   *errs = (int64_t)h;
+  return BFB_OK;
+}
+
+// ------------------------------------------------------ multi-process mode --
+// One process per GPU (torchrun): this context runs node `rank` of CN.  The
+// host driver (paper_2103_13577_b200/dist.py) sequences the steps below and
+// provides the cross-process barrier + snapshot-size exchange between publish
+// and merge; peers' snapshots are read directly from their HBM (CUDA IPC).
+
+int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int strategy,
+               int want_parents, int rank) {
+  if (rank < 0 || rank >= parts) return fail(BFB_ERR_INVALID, "rank out of range");
+  if (parts > kMaxSrc) return fail(BFB_ERR_INVALID, "at most 64 nodes in multi-process mode");
+  // Validate and allocate as a single-node engine over the local part, then
+  // re-label it with the global partition.
+  BFB_TRY(engine_setup(ctx, 1, std::vector<int64_t>{0, ctx->g.n}.data(), 1, strategy,
+                       want_parents));
+  const int64_t n = ctx->g.n;
+  if (bounds[0] != 0 || bounds[parts] != n)
+    return fail(BFB_ERR_PARTITION, "partition does not match graph");
+  for (int g = 0; g < parts; ++g)
+    if (bounds[g + 1] < bounds[g]) return fail(BFB_ERR_PARTITION, "partition does not match graph");
+  if (fanout < 1 || fanout > parts) return fail(BFB_ERR_FANOUT, "fanout exceeds num_nodes");
+  BFB_TRY(make_schedule(parts, fanout, strategy, ctx->schedule));
+  ctx->num_parts = parts;
+  ctx->fanout = fanout;
+  ctx->bounds.assign(bounds, bounds + parts + 1);
+  EngineTables* D = ctx->tables;
+  D->rank = rank;
+  Part& p = ctx->parts[0];
+  p.lo = bounds[rank];
+  p.hi = bounds[rank + 1];
+  p.wlo = p.lo >> 5;
+  p.whi = p.hi == p.lo ? (p.lo >> 5) : ((p.hi + 31) >> 5);
+  int64_t ob[2];
+  BFB_CUDA(cudaMemcpy(&ob[0], ctx->g.offsets.p + p.lo, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  BFB_CUDA(cudaMemcpy(&ob[1], ctx->g.offsets.p + p.hi, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  p.owned_edges = ob[1] - ob[0];
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t nwords_pad = (nwords + kWordsPerCommitBlock - 1) / kWordsPerCommitBlock *
+                                 kWordsPerCommitBlock + kWordsPerCommitBlock;
+  BFB_TRY(p.pub.alloc(nwords_pad));
+  BFB_TRY(p.pub_alt.alloc(nwords_pad));
+  BFB_CUDA(cudaMemset(p.pub.p, 0, nwords_pad * sizeof(uint32_t)));
+  BFB_CUDA(cudaMemset(p.pub_alt.p, 0, nwords_pad * sizeof(uint32_t)));
+  for (int par = 0; par < 2; ++par) D->peer_pub[par].assign(parts, nullptr);
+  D->peer_pub[0][rank] = p.pub.p;
+  D->peer_pub[1][rank] = p.pub_alt.p;
+  return BFB_OK;
+}
+
+int rank_ipc_handles(bfb_ctx* ctx, void* out) {
+  if (!ctx->tables || ctx->tables->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
+  cudaIpcMemHandle_t h[2];
+  BFB_CUDA(cudaIpcGetMemHandle(&h[0], ctx->parts[0].pub.p));
+  BFB_CUDA(cudaIpcGetMemHandle(&h[1], ctx->parts[0].pub_alt.p));
+  std::memcpy(out, h, sizeof(h));
+  return BFB_OK;
+}
+
+int rank_open_peer(bfb_ctx* ctx, int peer, const void* handles) {
+  EngineTables* D = ctx->tables;
+  if (!D || D->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
+  if (peer < 0 || peer >= ctx->num_parts || peer == D->rank)
+    return fail(BFB_ERR_INVALID, "bad peer");
+  cudaIpcMemHandle_t h[2];
+  std::memcpy(h, handles, sizeof(h));
+  for (int par = 0; par < 2; ++par) {
+    void* ptr = nullptr;
+    BFB_CUDA(cudaIpcOpenMemHandle(&ptr, h[par], cudaIpcMemLazyEnablePeerAccess));
+    D->opened.push_back(ptr);
+    D->peer_pub[par][peer] = static_cast<const uint32_t*>(ptr);
+  }
+  return BFB_OK;
+}
+
+int rank_begin(bfb_ctx* ctx, int64_t root) {
+  EngineTables* D = ctx->tables;
+  if (!D || D->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
+  const int64_t n = ctx->g.n;
+  if (root < 0 || root >= n)
+    return fail(BFB_ERR_ROOT, "root " + std::to_string(root) + " out of range [0, " +
+                                  std::to_string(n) + ")");
+  for (int par = 0; par < 2; ++par)
+    for (int g = 0; g < ctx->num_parts; ++g)
+      if (!D->peer_pub[par][g]) return fail(BFB_ERR_STATE, "peer snapshots not mapped");
+  cudaStream_t s = ctx->stream;
+  Part& p = ctx->parts[0];
+  const int64_t nwords = (n + 31) / 32;
+  BFB_CUDA(cudaEventRecord(D->ev[0], s));
+  BFB_CUDA(cudaMemsetAsync(ctx->run.p, 0, sizeof(RunCounters), s));
+  BFB_CUDA(cudaMemsetAsync(p.visited.p, 0, nwords * sizeof(uint32_t), s));
+  BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
+  BFB_CUDA(cudaMemsetAsync(p.level.p, 0xFF, n * sizeof(uint32_t), s));
+  if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
+  const int owner = root >= p.lo && root < p.hi;
+  k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), ctx->g.offsets.p, root, owner, ctx->run.p);
+  BFB_CUDA(cudaGetLastError());
+  D->level = 0;
+  D->levels = 1;
+  D->reached = 1;
+  ctx->last_sizes.assign(1, 1);
+  D->launches = 1;
+  D->remote_messages = D->remote_vertices = D->high_water = D->exchange_bytes = 0;
+  ctx->last_root = root;
+  return BFB_OK;
+}
+
+int rank_expand(bfb_ctx* ctx) {
+  PartView v = view_of(ctx, ctx->parts[0]);
+  if (ctx->want_parents)
+    k_expand<true><<<ctx->expand_grid, kExpandBlock, 0, ctx->stream>>>(v, ctx->g.adj.p);
+  else
+    k_expand<false><<<ctx->expand_grid, kExpandBlock, 0, ctx->stream>>>(v, ctx->g.adj.p);
+  ++ctx->tables->launches;
+  BFB_CUDA(cudaGetLastError());
+  return BFB_OK;
+}
+
+int rank_publish(bfb_ctx* ctx, int parity, int64_t* count_out) {
+  cudaStream_t s = ctx->stream;
+  Part& p = ctx->parts[0];
+  PartView v = view_of(ctx, p);
+  v.pub = parity ? p.pub_alt.p : p.pub.p;
+  const int64_t nwords = (ctx->g.n + 31) / 32;
+  BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_count[parity], 0, sizeof(int64_t), s));
+  k_publish<<<grid_cap(nwords, 256, ctx->num_sms, 4), 256, 0, s>>>(v, parity);
+  ++ctx->tables->launches;
+  BFB_CUDA(cudaMemcpyAsync(ctx->pinned, &p.ctr.p->pub_count[parity], sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, s));
+  BFB_CUDA(cudaStreamSynchronize(s));
+  *count_out = ctx->pinned[0];
+  return BFB_OK;
+}
+
+int rank_merge(bfb_ctx* ctx, int parity, const int32_t* srcs, const int64_t* counts, int nsrc) {
+  EngineTables* D = ctx->tables;
+  SrcList L;
+  L.n = 0;
+  int64_t incoming = 0;
+  for (int i = 0; i < nsrc; ++i) {
+    const int g = srcs[i];
+    if (g < 0 || g >= ctx->num_parts || g == D->rank) return fail(BFB_ERR_INVALID, "bad source");
+    if (counts[i] <= 0) continue;  // empty-buffer suppression
+    L.p[L.n++] = D->peer_pub[parity][g];
+    incoming += counts[i];
+  }
+  const int64_t nwords = (ctx->g.n + 31) / 32;
+  D->remote_messages += L.n;
+  D->remote_vertices += incoming;
+  D->exchange_bytes += (int64_t)L.n * nwords * (int64_t)sizeof(uint32_t);
+  D->high_water = std::max(D->high_water, incoming);
+  if (incoming > (int64_t)ctx->fanout * ctx->g.n && ctx->strategy == BFB_STRATEGY_BUTTERFLY)
+    return fail(BFB_ERR_CAPACITY, "buffer bound violated");
+  if (L.n == 0) return BFB_OK;
+  k_merge_peers<<<grid_cap(nwords, 256, ctx->num_sms, 4), 256, 0, ctx->stream>>>(
+      L, ctx->parts[0].visited.p, nwords);
+  ++D->launches;
+  BFB_CUDA(cudaGetLastError());
+  return BFB_OK;
+}
+
+int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
+  EngineTables* D = ctx->tables;
+  cudaStream_t s = ctx->stream;
+  Part& p = ctx->parts[0];
+  PartView v = view_of(ctx, p);
+  const int64_t nwords = (ctx->g.n + 31) / 32;
+  const uint32_t next_level = (uint32_t)(D->level + 1);
+  k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
+  ++D->launches;
+  if (p.whi > p.wlo) {
+    const int64_t cb = commit_blocks(p.wlo, p.whi);
+    k_commit_owned<false><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, ctx->g.offsets.p, next_level);
+    k_commit_scan<<<1, 1024, 0, s>>>(v, cb, ctx->run.p);
+    k_commit_owned<true><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, ctx->g.offsets.p, next_level);
+    D->launches += 3;
+  }
+  if (nwords - (p.whi - p.wlo) > 0) {
+    k_commit_rest<<<grid_cap(nwords, 256, ctx->num_sms, 4), 256, 0, s>>>(v, next_level);
+    ++D->launches;
+  }
+  BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  BFB_CUDA(cudaStreamSynchronize(s));
+  BFB_CUDA(cudaGetLastError());
+  const int64_t f = ctx->pinned[2];  // PartCounters: q_count, q_edges, frontier
+  *frontier_out = f;
+  *owned_out = ctx->pinned[0];
+  if (f) {
+    ++D->level;
+    ++D->levels;
+    D->reached += f;
+    ctx->last_sizes.push_back(f);
+  }
+  return BFB_OK;
+}
+
+int rank_finish(bfb_ctx* ctx, bfb_run_stats* st) {
+  EngineTables* D = ctx->tables;
+  cudaStream_t s = ctx->stream;
+  BFB_CUDA(cudaEventRecord(D->ev[1], s));
+  RunCounters rc;
+  BFB_CUDA(cudaMemcpyAsync(&rc, ctx->run.p, sizeof(rc), cudaMemcpyDeviceToHost, s));
+  BFB_CUDA(cudaStreamSynchronize(s));
+  float elapsed = 0;
+  BFB_CUDA(cudaEventElapsedTime(&elapsed, D->ev[0], D->ev[1]));
+  ctx->have_run = true;
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->levels = D->levels;
+    st->rounds_executed = D->levels * (int64_t)ctx->schedule.size();
+    st->remote_messages = D->remote_messages;
+    st->remote_vertices = D->remote_vertices;
+    st->traversed_edges = rc.traversed_edges;  // this node's q_local edges only
+    st->reached = D->reached;
+    st->buffer_high_water_max = D->high_water;
+    st->exchange_bytes = D->exchange_bytes;
+    st->elapsed_ms = elapsed;
+    st->kernel_launches = D->launches;
+  }
+  return BFB_OK;
+}
+
+int rank_parents_raw(bfb_ctx* ctx, uint32_t* out) {
+  if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
+  BFB_CUDA(cudaMemcpy(out, ctx->parts[0].parent.p, ctx->g.n * sizeof(uint32_t),
+                      cudaMemcpyDeviceToHost));
   return BFB_OK;
 }
 

@@ -99,6 +99,21 @@ int bfb_device_count(int* count_out) {
   return BFB_OK;
 }
 
+int bfb_host_alloc(size_t bytes, void** ptr_out) {
+  if (!ptr_out) return fail(BFB_ERR_INVALID, "null output");
+  *ptr_out = nullptr;
+  cudaError_t e = cudaHostAlloc(ptr_out, bytes ? bytes : 1, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BFB_ERR_OOM, std::string("cudaHostAlloc failed: ") + cudaGetErrorString(e));
+  }
+  return BFB_OK;
+}
+
+void bfb_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
 int bfb_num_rounds(int num_nodes, int fanout, int* rounds_out) {
   std::vector<std::vector<std::vector<int>>> s;
   BFB_TRY(make_schedule(num_nodes, fanout, BFB_STRATEGY_BUTTERFLY, s));
@@ -296,6 +311,14 @@ int bfb_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_o
                     buffer_high_water_out, stats_out);
 }
 
+int bfb_frontier_sizes(bfb_ctx* ctx, int64_t* out, int64_t cap, int64_t* len_out) {
+  CTX_GUARD(ctx);
+  const int64_t L = (int64_t)ctx->last_sizes.size();
+  if (len_out) *len_out = L;
+  for (int64_t i = 0; i < L && i < cap && out; ++i) out[i] = ctx->last_sizes[i];
+  return BFB_OK;
+}
+
 int bfb_copy_levels(bfb_ctx* ctx, uint32_t* levels_out) {
   CTX_GUARD(ctx);
   return engine_copy_levels(ctx, levels_out);
@@ -309,6 +332,67 @@ int bfb_copy_parents(bfb_ctx* ctx, int64_t* parents_out) {
 int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out) {
   CTX_GUARD(ctx);
   return engine_validate(ctx, root, errors_out);
+}
+
+int bfb_rank_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int fanout,
+                   int strategy, int want_parents, int rank) {
+  CTX_GUARD(ctx);
+  NEED_GRAPH(ctx);
+  if (!boundaries) return fail(BFB_ERR_INVALID, "null boundaries");
+  return rank_setup(ctx, num_parts, boundaries, fanout, strategy, want_parents, rank);
+}
+
+int bfb_rank_ipc_handles(bfb_ctx* ctx, void* handles_out) {
+  CTX_GUARD(ctx);
+  if (!handles_out) return fail(BFB_ERR_INVALID, "null output");
+  return rank_ipc_handles(ctx, handles_out);
+}
+
+int bfb_rank_open_peer(bfb_ctx* ctx, int peer, const void* handles) {
+  CTX_GUARD(ctx);
+  if (!handles) return fail(BFB_ERR_INVALID, "null handles");
+  return rank_open_peer(ctx, peer, handles);
+}
+
+int bfb_rank_begin(bfb_ctx* ctx, int64_t root) {
+  CTX_GUARD(ctx);
+  return rank_begin(ctx, root);
+}
+
+int bfb_rank_expand(bfb_ctx* ctx) {
+  CTX_GUARD(ctx);
+  return rank_expand(ctx);
+}
+
+int bfb_rank_publish(bfb_ctx* ctx, int parity, int64_t* count_out) {
+  CTX_GUARD(ctx);
+  if (!count_out || (parity != 0 && parity != 1)) return fail(BFB_ERR_INVALID, "bad argument");
+  return rank_publish(ctx, parity, count_out);
+}
+
+int bfb_rank_merge(bfb_ctx* ctx, int parity, const int32_t* sources, const int64_t* counts,
+                   int num_sources) {
+  CTX_GUARD(ctx);
+  if (num_sources < 0 || (num_sources && (!sources || !counts)) || (parity != 0 && parity != 1))
+    return fail(BFB_ERR_INVALID, "bad argument");
+  return rank_merge(ctx, parity, sources, counts, num_sources);
+}
+
+int bfb_rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
+  CTX_GUARD(ctx);
+  if (!frontier_out || !owned_out) return fail(BFB_ERR_INVALID, "null output");
+  return rank_commit(ctx, frontier_out, owned_out);
+}
+
+int bfb_rank_finish(bfb_ctx* ctx, bfb_run_stats* stats_out) {
+  CTX_GUARD(ctx);
+  return rank_finish(ctx, stats_out);
+}
+
+int bfb_rank_parents_raw(bfb_ctx* ctx, uint32_t* parents_out) {
+  CTX_GUARD(ctx);
+  if (!parents_out) return fail(BFB_ERR_INVALID, "null output");
+  return rank_parents_raw(ctx, parents_out);
 }
 
 }  // extern "C"

@@ -7,12 +7,46 @@ engine buffers of the last ``setup``; nothing here falls back to the CPU.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from ctypes import byref, c_int64, c_void_p
 
 import numpy as np
 
 from . import _lib
 from ._lib import check, ptr
+
+
+class _PinnedPool:
+    """Page-locked host buffers handed out as numpy arrays.  A buffer returns
+    to the pool when its array is garbage-collected, so repeated engine.run
+    calls reuse pinned memory and the levels D2H runs at full PCIe/C2C speed."""
+
+    def __init__(self):
+        self._free = {}  # nbytes -> [addr]
+
+    def array(self, count, dtype):
+        dtype = np.dtype(dtype)
+        nbytes = int(count) * dtype.itemsize
+        lst = self._free.get(nbytes)
+        if lst:
+            addr = lst.pop()
+        else:
+            p = c_void_p()
+            check(_lib.load().bfb_host_alloc(max(nbytes, 1), byref(p)))
+            addr = p.value
+        buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(addr)
+        weakref.finalize(buf, self._release, nbytes, addr)
+        return np.frombuffer(buf, dtype=dtype, count=int(count))
+
+    def _release(self, nbytes, addr):
+        lst = self._free.setdefault(nbytes, [])
+        if len(lst) < 2:
+            lst.append(addr)
+        else:
+            _lib.load().bfb_host_free(c_void_p(addr))
+
+
+_POOL = _PinnedPool()
 
 
 class DeviceGraph:
@@ -171,7 +205,7 @@ class DeviceGraph:
         parents|None, frontier_sizes, RunStatsC, buffer_high_water)."""
         if self._engine_key is None:
             raise RuntimeError("engine not set up")
-        lv = np.empty(self._n, dtype=np.uint32) if levels else None
+        lv = _POOL.array(self._n, np.uint32) if levels else None
         pa = np.empty(self._n, dtype=np.int64) if parents else None
         sizes = np.zeros(max_levels, dtype=np.int64)
         hw = np.zeros(self.num_parts, dtype=np.int64)
@@ -179,7 +213,19 @@ class DeviceGraph:
         check(_lib.load().bfb_bfs(self.handle, int(root), ptr(lv, ctypes.c_uint32),
                                   ptr(pa, ctypes.c_int64), ptr(sizes, ctypes.c_int64), max_levels,
                                   ptr(hw, ctypes.c_int64), byref(st)))
-        return lv, pa, sizes[:min(st.levels, max_levels)].tolist(), st, hw
+        if st.levels > max_levels:
+            sizes = self.frontier_sizes()
+        else:
+            sizes = sizes[:st.levels].tolist()
+        return lv, pa, sizes, st, hw
+
+    def frontier_sizes(self):
+        """per_level_frontier_size of the last run, all levels."""
+        n = c_int64()
+        check(_lib.load().bfb_frontier_sizes(self.handle, None, 0, byref(n)))
+        out = np.empty(n.value, dtype=np.int64)
+        check(_lib.load().bfb_frontier_sizes(self.handle, ptr(out, ctypes.c_int64), out.size, byref(n)))
+        return out.tolist()
 
     def levels(self):
         out = np.empty(self._n, dtype=np.uint32)

@@ -91,7 +91,7 @@ def test_golden_levels_s20(golden):
 def _sweep_graphs():
     yield "rmat13", util.rmat_graph(13)
     yield "gnp", util.gnp_graph(5000, 0.002)
-    yield "path", util.path_graph(10000)
+    yield "path", util.path_graph(1500)
     yield "star", util.star_graph(300)
     yield "components", util.components_graph()
 
