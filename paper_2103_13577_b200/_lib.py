@@ -15,7 +15,8 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint3
 import numpy as np
 
 LIB_NAME = "libbflybfs.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        os.environ.get("BFB_LIB", LIB_NAME))  # BFB_LIB: tuning-build override
 
 BFB_OK = 0
 ERR_INVALID, ERR_ROOT, ERR_PARTITION, ERR_FANOUT = -1, -2, -3, -4

@@ -33,12 +33,9 @@ constexpr int kExpandBlock = 256;
 constexpr int kExpandItems = 8;
 constexpr int64_t kTile = (int64_t)kExpandBlock * kExpandItems;  // edges per tile
 constexpr int kCommitBlock = 256;
-constexpr int64_t kWordsPerCommitBlock = 1024;                    // 32768 vertices
-
-// Commit blocks of a part: word range [wlo & ~31, whi) in 1024-word blocks.
-__host__ __device__ inline int64_t commit_blocks(int64_t wlo, int64_t whi) {
-  return (whi - (wlo & ~(int64_t)31) + kWordsPerCommitBlock - 1) / kWordsPerCommitBlock;
-}
+constexpr int kScanItems = 16;                 // commit unit scan: units per thread
+constexpr int64_t kScanTile = 256 * kScanItems;
+constexpr int64_t kWordPad = 1024;  // bitmap allocation padding (words)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct PartView {
@@ -50,10 +47,12 @@ struct PartView {
   uint32_t* pub;
   uint32_t* q_v;
   int64_t* q_pre;
-  int64_t* q_row;
   uint32_t* tile_vstart;
-  int64_t* block_sums;
+  int64_t abase, nunits;  // commit units: words [abase, abase + 32 * nunits)
+  uint32_t* ucnt;
+  int64_t *udeg, *upos, *uepre, *tcnt, *tdeg;
   PartCounters* ctr;
+  const int64_t* off;  // CSR offsets (rows of q_v)
 };
 
 PartView view_of(bfb_ctx* ctx, Part& p) {
@@ -70,10 +69,18 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.pub = p.pub.p;
   v.q_v = p.q_v.p;
   v.q_pre = p.q_pre.p;
-  v.q_row = p.q_row.p;
   v.tile_vstart = p.tile_vstart.p;
-  v.block_sums = p.block_sums.p;
+  v.abase = p.wlo & ~(int64_t)31;
+  v.nunits = p.whi > p.wlo ? (p.whi - v.abase + 31) / 32 : 0;
+  const int64_t nu = v.nunits + 1, nt = (v.nunits + kScanTile - 1) / kScanTile + 1;
+  v.ucnt = p.unit_u32.p;
+  v.udeg = p.unit_i64.p;
+  v.upos = v.udeg + nu;
+  v.uepre = v.upos + nu;
+  v.tcnt = v.uepre + nu;
+  v.tdeg = v.tcnt + nt;
   v.ctr = p.ctr.p;
+  v.off = ctx->g.offsets.p;
   return v;
 }
 
@@ -92,7 +99,6 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
       int64_t d = off[root + 1] - off[root];
       v.q_v[0] = (uint32_t)root;
       v.q_pre[0] = 0;
-      v.q_row[0] = off[root];
       c.q_count = 1;
       c.q_edges = d;
       atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)d);
@@ -107,18 +113,50 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
 }
 
 // ------------------------------------------------------------ phase 1 ----
-// One 2048-edge tile per block iteration (load-balanced search).  The tile's
-// frontier segment is staged in shared memory as adjacency bases (row start
-// minus edge prefix).  Each edge finds its vertex either by binary search over
-// the segments' first edges (few segments: hub tiles) or through an owner map
-// built by scattering segment starts and a block max-scan (many segments:
-// low-degree tiles).  Small staging keeps more of the unified L1 for probes.
-constexpr int kSearchMax = 16;
+// Probe the visited bitmap for each gathered neighbour and claim the unvisited
+// ones (check-and-set).  Without parents a fire-and-forget
+// red.or suffices (the commit pass finds the new bits); with parents the
+// atomic's old value elects one winner per vertex, which writes the parent.
+template <bool kParents>
+__device__ __forceinline__ void claim_batch(const uint32_t (&u)[kExpandItems],
+                                            const uint32_t (&src)[kExpandItems], unsigned okmask,
+                                            uint32_t* __restrict__ visited,
+                                            uint32_t* __restrict__ parent) {
+  uint32_t wv[kExpandItems];
+#pragma unroll
+  for (int it = 0; it < kExpandItems; ++it)
+    if ((okmask >> it) & 1u) wv[it] = visited[u[it] >> 5];
+#pragma unroll
+  for (int it = 0; it < kExpandItems; ++it) {
+    if ((okmask >> it) & 1u) {
+      const uint32_t bit = 1u << (u[it] & 31);
+      if (!(wv[it] & bit)) {
+        if (kParents) {
+          if (!(atomicOr(&visited[u[it] >> 5], bit) & bit)) parent[u[it]] = src[it];
+        } else {
+          atomicOr(&visited[u[it] >> 5], bit);
+        }
+      }
+    }
+  }
+}
+
+// Phase 1: one 2048-edge tile per block iteration (load-balanced search over
+// the frontier's degree prefix).  Tiles inside at most kRegSegs frontier rows
+// (hub rows, most of the edges on Kronecker graphs) resolve each edge's row
+// from registers with no shared memory and no block barrier.  Tiles spanning
+// many low-degree rows stage the rows' adjacency bases in shared memory and
+// build an edge -> row owner map (scatter of row starts + block max-scan).
+constexpr int kRegSegs = 4;
+#ifndef BFB_EXPAND_MINB
+#define BFB_EXPAND_MINB 4
+#endif
+constexpr int kExpandMinBlocks = BFB_EXPAND_MINB;  // 4: 64-register cap, 32 warps per SM
 
 template <bool kParents>
-__global__ void __launch_bounds__(kExpandBlock) k_expand(PartView v,
+__global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartView v,
                                                          const uint32_t* __restrict__ adj) {
-  __shared__ int32_t s_idx[kTile + 1];   // segment first edges (search) or owner map
+  __shared__ int32_t s_own[kTile];
   __shared__ int64_t s_base[kTile + 1];
   __shared__ uint32_t s_v[kParents ? kTile + 1 : 1];
   __shared__ int32_t s_wmax[kExpandBlock / 32];
@@ -134,30 +172,63 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand(PartView v,
     const int64_t vs = v.tile_vstart[t];
     const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
     const int nseg = (int)(ve - vs + 1);
-    const bool use_map = nseg > kSearchMax;
-    if (use_map) {
-      for (int k = threadIdx.x; k < kTile; k += kExpandBlock) s_idx[k] = 0;
-      __syncthreads();
+    uint32_t u[kExpandItems], src[kExpandItems];
+    unsigned ok = 0;
+    if (nseg <= kRegSegs) {
+      int32_t rel[kRegSegs];
+      int64_t base[kRegSegs];
+      uint32_t sv[kRegSegs];
+#pragma unroll
+      for (int k = 0; k < kRegSegs; ++k) {
+        rel[k] = INT32_MAX;
+        base[k] = 0;
+        sv[k] = 0;
+        if (k < nseg) {
+          const int64_t pre = __ldg(v.q_pre + vs + k);
+          rel[k] = (int32_t)max(pre - e0, (int64_t)INT32_MIN);
+          const uint32_t qv = __ldg(v.q_v + vs + k);
+          base[k] = __ldg(v.off + qv) - pre;
+          sv[k] = qv;
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < kExpandItems; ++it) {
+        const int r = it * kExpandBlock + threadIdx.x;
+        if (r < span) {
+          int64_t b = base[0];
+          uint32_t s0 = sv[0];
+#pragma unroll
+          for (int k = 1; k < kRegSegs; ++k)
+            if (r >= rel[k]) {
+              b = base[k];
+              s0 = sv[k];
+            }
+          u[it] = ld_stream_u32(adj + b + e0 + r);
+          src[it] = s0;
+          ok |= 1u << it;
+        }
+      }
+      claim_batch<kParents>(u, src, ok, visited, v.parent);
+      continue;
     }
+    for (int k = threadIdx.x; k < kTile; k += kExpandBlock) s_own[k] = 0;
+    __syncthreads();
     for (int k = threadIdx.x; k < nseg; k += kExpandBlock) {
       const int64_t pre = v.q_pre[vs + k];
-      s_base[k] = v.q_row[vs + k] - pre;
-      if (kParents) s_v[k] = v.q_v[vs + k];
-      if (use_map) {
-        const int64_t r = pre - e0;
-        if (r > 0 && r < span) s_idx[r] = k;
-      } else {
-        s_idx[k] = (int32_t)max(pre - e0, (int64_t)INT32_MIN);
-      }
+      const uint32_t qv = v.q_v[vs + k];
+      s_base[k] = __ldg(v.off + qv) - pre;
+      if (kParents) s_v[k] = qv;
+      const int64_t r = pre - e0;
+      if (r > 0 && r < span) s_own[r] = k;
     }
     __syncthreads();
-    if (use_map) {  // inclusive max-scan of the owner map, 8 entries per thread
+    {  // inclusive max-scan of the owner map, kTile / kExpandBlock entries per thread
       constexpr int kPer = kTile / kExpandBlock;
       int32_t loc[kPer];
       int32_t run = 0;
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
-        run = max(run, s_idx[threadIdx.x * kPer + i]);
+        run = max(run, s_own[threadIdx.x * kPer + i]);
         loc[i] = run;
       }
       int32_t inc = run;
@@ -170,47 +241,23 @@ __global__ void __launch_bounds__(kExpandBlock) k_expand(PartView v,
       __syncthreads();
       int32_t carry = 0;
       for (int w = 0; w < warp; ++w) carry = max(carry, s_wmax[w]);
-      const int32_t prev = max(carry, __shfl_up_sync(0xffffffffu, inc, 1) * (lane > 0));
+      const int32_t up = __shfl_up_sync(0xffffffffu, inc, 1);
+      const int32_t prev = max(carry, lane > 0 ? up : 0);
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) s_idx[threadIdx.x * kPer + i] = max(prev, loc[i]);
+      for (int i = 0; i < kPer; ++i) s_own[threadIdx.x * kPer + i] = max(prev, loc[i]);
       __syncthreads();
     }
-    uint32_t u[kExpandItems];
-    int seg[kExpandItems];
 #pragma unroll
     for (int it = 0; it < kExpandItems; ++it) {
       const int r = it * kExpandBlock + threadIdx.x;
-      seg[it] = -1;
       if (r < span) {
-        int lo;
-        if (use_map) {
-          lo = s_idx[r];
-        } else {
-          lo = 0;
-          int hi = nseg - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_idx[mid] <= r) lo = mid; else hi = mid - 1;
-          }
-        }
-        seg[it] = lo;
-        u[it] = ld_stream_u32(adj + s_base[lo] + e0 + r);
+        const int sg = s_own[r];
+        u[it] = ld_stream_u32(adj + s_base[sg] + e0 + r);
+        src[it] = kParents ? s_v[sg] : 0u;
+        ok |= 1u << it;
       }
     }
-    uint32_t wv[kExpandItems];
-#pragma unroll
-    for (int it = 0; it < kExpandItems; ++it)
-      if (seg[it] >= 0) wv[it] = visited[u[it] >> 5];
-#pragma unroll
-    for (int it = 0; it < kExpandItems; ++it) {
-      if (seg[it] >= 0) {
-        const uint32_t bit = 1u << (u[it] & 31);
-        if (!(wv[it] & bit)) {
-          atomicOr(&visited[u[it] >> 5], bit);
-          if (kParents) v.parent[u[it]] = s_v[seg[it]];
-        }
-      }
-    }
+    claim_batch<kParents>(u, src, ok, visited, v.parent);
     __syncthreads();
   }
 }
@@ -303,163 +350,95 @@ __device__ __forceinline__ uint32_t owned_mask(int64_t w, int64_t lo, int64_t hi
   return mask;
 }
 
-// Sum of degrees of the owned new vertices held in own[] (lane = bit), with
-// kCommitBatch words' offsets loads in flight per iteration.
-constexpr int kCommitBatch = 8;
-
-template <int kChunks>
-__device__ __forceinline__ int64_t commit_degree_sum(const uint32_t (&own)[kChunks], int64_t wbase,
-                                                     int lane, const int64_t* __restrict__ off) {
-  int64_t deg = 0;
-#pragma unroll
-  for (int c = 0; c < kChunks; ++c) {
-    const unsigned m = __ballot_sync(0xffffffffu, own[c] != 0);
-#pragma unroll 1
-    for (int g8 = 0; g8 < 32; g8 += kCommitBatch) {
-      if (!((m >> g8) & ((1u << kCommitBatch) - 1u))) continue;
-#pragma unroll
-      for (int k = 0; k < kCommitBatch; ++k) {
-        const uint32_t x = __shfl_sync(0xffffffffu, own[c], g8 + k);
-        if ((x >> lane) & 1u) {
-          const int64_t u = ((wbase + c * 32 + g8 + k) << 5) + lane;
-          deg += __ldg(off + u + 1) - __ldg(off + u);
-        }
-      }
-    }
-  }
-  return deg;
+// Commit of the owned words, in warp units of 32 words (1024 vertices):
+//   k_commit_count  per unit: owned new vertices and their degree sum
+//   k_unit_scan_*   device-wide exclusive scan of the (count, degree) pairs
+//   k_commit_write  per unit, from its prefix: levels, q_v, q_pre, tile
+//                   starts, start snapshot -- q_local in ascending order
+// Thread = word: each lane walks the set bits of its own word (independent
+// offsets loads, high MLP, no block barriers); one warp scan per unit turns
+// per-word (count, degree) into positions.
+__device__ __forceinline__ void unit_word(const PartView& v, int64_t unit, int lane, uint32_t& a,
+                                          uint32_t& nb, uint32_t& own) {
+  const int64_t w = v.abase + unit * 32 + lane;
+  const bool in = w >= v.wlo && w < v.whi;
+  a = in ? v.visited[w] : 0u;
+  nb = a & ~(in ? v.start[w] : 0u);
+  own = nb & owned_mask(w, v.lo, v.hi);
 }
 
-// Commit of the owned words, as reduce (kWrite = false) -> scan -> write
-// (kWrite = true) over 1024-word blocks.  Lane l of a warp holds word
-// (chunk base + l) of each chunk; vertex work then runs with lane = bit, so
-// offsets reads, level writes and queue writes are coalesced.  The reduce
-// pass stores (owned new vertices, their degree sum) per block; the write
-// pass recomputes them and emits q_local in ascending vertex order.
-template <bool kWrite>
-__global__ void __launch_bounds__(kCommitBlock) k_commit_owned(PartView v,
-                                                               const int64_t* __restrict__ off,
-                                                               uint32_t next_level) {
-  constexpr int kWarps = kCommitBlock / 32;
-  constexpr int kChunks = kWordsPerCommitBlock / kCommitBlock;  // words per lane
-  __shared__ int64_t s_wcnt[kWarps], s_wdeg[kWarps];
+__device__ __forceinline__ int64_t word_degree_sum(uint32_t x, int64_t vbase,
+                                                   const int64_t* __restrict__ off) {
+  int64_t d = 0;
+  while (x) {
+    const int b = __ffs(x) - 1;
+    x &= x - 1;
+    d += __ldg(off + vbase + b + 1) - __ldg(off + vbase + b);
+  }
+  return d;
+}
+
+__global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t* __restrict__ off) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t fr = 0;
+  for (int64_t unit = gw; unit < v.nunits; unit += nw) {
+    uint32_t a, nb, own;
+    unit_word(v, unit, lane, a, nb, own);
+    fr += __popc(nb);
+    const uint32_t c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(own));
+    int64_t d = 0;
+    if (c) d = warp_sum_i64(word_degree_sum(own, (v.abase + unit * 32 + lane) << 5, off));
+    if (lane == 0) {
+      v.ucnt[unit] = c;
+      v.udeg[unit] = d;
+    }
+  }
   __shared__ int64_t red[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t bid = blockIdx.x;
-  const int64_t wbase = (v.wlo & ~(int64_t)31) + bid * kWordsPerCommitBlock +
-                        (int64_t)warp * (kChunks * 32);
-  uint32_t nb[kChunks], own[kChunks], vis[kChunks];
-  int64_t cnt = 0, fr = 0;
-#pragma unroll
-  for (int c = 0; c < kChunks; ++c) {
-    const int64_t w = wbase + c * 32 + lane;
-    const bool in = w >= v.wlo && w < v.whi;
-    const uint32_t a = in ? v.visited[w] : 0u;
-    const uint32_t s0 = in ? v.start[w] : 0u;
-    vis[c] = a;
-    nb[c] = a & ~s0;
-    own[c] = nb[c] & owned_mask(w, v.lo, v.hi);
-    cnt += __popc(own[c]);
-    fr += __popc(nb[c]);
-  }
-  if (!kWrite) {
-    int64_t deg = commit_degree_sum<kChunks>(own, wbase, lane, off);
-    cnt = block_sum_i64(cnt, red);
-    deg = block_sum_i64(deg, red);
-    fr = block_sum_i64(fr, red);
-    if (threadIdx.x == 0) {
-      v.block_sums[2 * bid] = cnt;
-      v.block_sums[2 * bid + 1] = deg;
-      if (fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
-    }
-    return;
-  }
-  // write pass: per-warp prefix inside the block, block prefix from the scan
-  int64_t deg = commit_degree_sum<kChunks>(own, wbase, lane, off);
-  cnt = warp_sum_i64(cnt);
-  deg = warp_sum_i64(deg);
-  if (lane == 0) {
-    s_wcnt[warp] = cnt;
-    s_wdeg[warp] = deg;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int64_t c = lane < kWarps ? s_wcnt[lane] : 0, d = lane < kWarps ? s_wdeg[lane] : 0;
-    const int64_t ic = warp_inclusive_i64(c), id = warp_inclusive_i64(d);
-    if (lane < kWarps) {
-      s_wcnt[lane] = ic - c + v.block_sums[2 * bid];
-      s_wdeg[lane] = id - d + v.block_sums[2 * bid + 1];
+  fr = block_sum_i64(fr, red);
+  if (threadIdx.x == 0 && fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+}
+
+__global__ void __launch_bounds__(256) k_unit_scan_reduce(PartView v) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int64_t c = 0, d = 0;
+#pragma unroll 4
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + (int64_t)k * 256 + threadIdx.x;
+    if (i < v.nunits) {
+      c += v.ucnt[i];
+      d += v.udeg[i];
     }
   }
-  __syncthreads();
-  int64_t pos = s_wcnt[warp];
-  int64_t epre = s_wdeg[warp];
-  const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int c = 0; c < kChunks; ++c) {
-    const unsigned m = __ballot_sync(0xffffffffu, nb[c] != 0);
-#pragma unroll 1
-    for (int g8 = 0; g8 < 32; g8 += kCommitBatch) {
-      if (!((m >> g8) & ((1u << kCommitBatch) - 1u))) continue;
-      uint32_t x[kCommitBatch], xo[kCommitBatch];
-      int64_t r0[kCommitBatch], d[kCommitBatch];
-#pragma unroll
-      for (int k = 0; k < kCommitBatch; ++k) {  // batch the offsets loads (MLP)
-        x[k] = __shfl_sync(0xffffffffu, nb[c], g8 + k);
-        xo[k] = __shfl_sync(0xffffffffu, own[c], g8 + k);
-        const int64_t u = ((wbase + c * 32 + g8 + k) << 5) + lane;
-        r0[k] = 0;
-        d[k] = 0;
-        if ((xo[k] >> lane) & 1u) {
-          r0[k] = __ldg(off + u);
-          d[k] = __ldg(off + u + 1) - r0[k];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kCommitBatch; ++k) {
-        const int64_t u = ((wbase + c * 32 + g8 + k) << 5) + lane;
-        if ((x[k] >> lane) & 1u) v.level[u] = next_level;
-        if (xo[k]) {
-          const bool has = (xo[k] >> lane) & 1u;
-          const int64_t dinc = warp_inclusive_i64(d[k]);
-          if (has) {
-            const int64_t p = pos + __popc(xo[k] & lt);
-            const int64_t e = epre + dinc - d[k];
-            v.q_v[p] = (uint32_t)u;
-            v.q_pre[p] = e;
-            v.q_row[p] = r0[k];
-            for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d[k]; ++t)
-              v.tile_vstart[t] = (uint32_t)p;
-          }
-          pos += __popc(xo[k]);
-          epre += __shfl_sync(0xffffffffu, dinc, 31);
-        }
-      }
-    }
-    const int64_t w = wbase + c * 32 + lane;
-    if (nb[c] && w >= v.wlo && w < v.whi) v.start[w] = vis[c];
+  __shared__ int64_t red[32];
+  c = block_sum_i64(c, red);
+  d = block_sum_i64(d, red);
+  if (threadIdx.x == 0) {
+    v.tcnt[blockIdx.x] = c;
+    v.tdeg[blockIdx.x] = d;
   }
 }
 
-// Exclusive scan of the per-block (count, degree) pairs in place; totals
-// become the next level's q_local size and edge count.
-__global__ void __launch_bounds__(1024) k_commit_scan(PartView v, int64_t nblocks,
-                                                      RunCounters* run) {
+// Single block: exclusive scan of the tile sums; totals -> next q_local size
+// and edge count (and RunStats.traversed_edges).
+__global__ void __launch_bounds__(1024) k_unit_scan_tiles(PartView v, int64_t ntiles,
+                                                          RunCounters* run) {
   __shared__ int64_t wsum[33];
   __shared__ int64_t carry_c, carry_d;
   if (threadIdx.x == 0) carry_c = carry_d = 0;
   __syncthreads();
-  for (int64_t base = 0; base < nblocks; base += blockDim.x) {
+  for (int64_t base = 0; base < ntiles; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    const int64_t c = i < nblocks ? v.block_sums[2 * i] : 0;
-    const int64_t d = i < nblocks ? v.block_sums[2 * i + 1] : 0;
+    const int64_t c = i < ntiles ? v.tcnt[i] : 0;
+    const int64_t d = i < ntiles ? v.tdeg[i] : 0;
     int64_t tc, td;
     const int64_t ec = block_exclusive_i64(c, wsum, &tc);
     const int64_t ed = block_exclusive_i64(d, wsum, &td);
     const int64_t cc = carry_c, cd = carry_d;
-    if (i < nblocks) {
-      v.block_sums[2 * i] = cc + ec;
-      v.block_sums[2 * i + 1] = cd + ed;
+    if (i < ntiles) {
+      v.tcnt[i] = cc + ec;
+      v.tdeg[i] = cd + ed;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -472,6 +451,77 @@ __global__ void __launch_bounds__(1024) k_commit_scan(PartView v, int64_t nblock
     v.ctr->q_count = carry_c;
     v.ctr->q_edges = carry_d;
     atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)carry_d);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_unit_scan_apply(PartView v) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t c[kScanItems], d[kScanItems];
+  int64_t sc = 0, sd = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k;
+    c[k] = i < v.nunits ? (int64_t)v.ucnt[i] : 0;
+    d[k] = i < v.nunits ? v.udeg[i] : 0;
+    sc += c[k];
+    sd += d[k];
+  }
+  __shared__ int64_t wsum[33];
+  int64_t tc, td;
+  int64_t ec = block_exclusive_i64(sc, wsum, &tc) + v.tcnt[blockIdx.x];
+  int64_t ed = block_exclusive_i64(sd, wsum, &td) + v.tdeg[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k;
+    if (i < v.nunits) {
+      v.upos[i] = ec;
+      v.uepre[i] = ed;
+    }
+    ec += c[k];
+    ed += d[k];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
+                                                      uint32_t next_level) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t unit = gw; unit < v.nunits; unit += nw) {
+    uint32_t a, nb, own;
+    unit_word(v, unit, lane, a, nb, own);
+    if (!__any_sync(0xffffffffu, nb != 0)) continue;
+    const int64_t w = v.abase + unit * 32 + lane;
+    const int64_t vbase = w << 5;
+    const int64_t dsum = own ? word_degree_sum(own, vbase, off) : 0;
+    const int cnt = __popc(own);
+    int cinc = cnt;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, cinc, dd);
+      if (lane >= dd) cinc += t;
+    }
+    const int64_t dinc = warp_inclusive_i64(dsum);
+    int64_t pos = v.upos[unit] + (cinc - cnt);
+    int64_t epre = v.uepre[unit] + (dinc - dsum);
+    uint32_t x = nb;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      const int64_t u = vbase + b;
+      v.level[u] = next_level;
+      if ((own >> b) & 1u) {
+        const int64_t r0 = __ldg(off + u);
+        const int64_t d = __ldg(off + u + 1) - r0;
+        v.q_v[pos] = (uint32_t)u;
+        v.q_pre[pos] = epre;
+        for (int64_t t = (epre + kTile - 1) / kTile; t * kTile < epre + d; ++t)
+          v.tile_vstart[t] = (uint32_t)pos;
+        ++pos;
+        epre += d;
+      }
+    }
+    if (nb) v.start[w] = a;
   }
 }
 
@@ -585,6 +635,19 @@ __global__ void k_merge_peers(SrcList L, uint32_t* __restrict__ vis, int64_t nwo
   }
 }
 
+// Owned-words commit (count -> pair scan -> write); returns kernels launched.
+int launch_commit(const PartView& v, const int64_t* off, uint32_t next_level, RunCounters* run,
+                  int sms, cudaStream_t s) {
+  const int64_t ntiles = std::max<int64_t>(1, (v.nunits + kScanTile - 1) / kScanTile);
+  const unsigned grid = grid_cap(v.nunits * 32, 256, sms, 8);
+  k_commit_count<<<grid, 256, 0, s>>>(v, off);
+  k_unit_scan_reduce<<<(unsigned)ntiles, 256, 0, s>>>(v);
+  k_unit_scan_tiles<<<1, 1024, 0, s>>>(v, ntiles, run);
+  k_unit_scan_apply<<<(unsigned)ntiles, 256, 0, s>>>(v);
+  k_commit_write<<<grid, 256, 0, s>>>(v, off, next_level);
+  return 5;
+}
+
 }  // namespace
 
 // Device-side tables built at setup (pointer arrays indexed by node, the
@@ -608,6 +671,29 @@ struct EngineTables {
       if (e) cudaEventDestroy(e);
   }
 };
+
+// L2 persistence window over the visited bitmap (BFB_L2_PERSIST=1): the
+// random probes then hit a bitmap that the streaming adjacency reads
+// (evict-first) cannot push out of the 126 MB L2.
+static int set_l2_window(bfb_ctx* ctx, void* base, size_t bytes) {
+  const char* e = std::getenv("BFB_L2_PERSIST");
+  if (!e || std::atoi(e) == 0) return BFB_OK;
+  int max_persist = 0, max_window = 0;
+  BFB_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+  BFB_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+  if (max_persist <= 0 || max_window <= 0) return BFB_OK;
+  const size_t carve = std::min(bytes, (size_t)max_persist);
+  BFB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+  cudaStreamAttrValue attr = {};
+  attr.accessPolicyWindow.base_ptr = base;
+  attr.accessPolicyWindow.num_bytes = std::min(bytes, (size_t)max_window);
+  attr.accessPolicyWindow.hitRatio =
+      std::min(1.0f, (float)carve / (float)attr.accessPolicyWindow.num_bytes);
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  BFB_CUDA(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+  return BFB_OK;
+}
 
 void engine_release(bfb_ctx* ctx) {
   ctx->parts.clear();
@@ -646,8 +732,7 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
   ctx->tables = new EngineTables();
   EngineTables* D = ctx->tables;
   const int64_t nwords = (n + 31) / 32;
-  const int64_t nwords_pad = (nwords + kWordsPerCommitBlock - 1) / kWordsPerCommitBlock *
-                                 kWordsPerCommitBlock + kWordsPerCommitBlock;
+  const int64_t nwords_pad = (nwords + kWordPad - 1) / kWordPad * kWordPad + kWordPad;
   std::vector<int64_t> off_h(parts + 1);
   {
     // owned edge counts: offsets at the boundaries
@@ -675,10 +760,13 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     if (parts > 1) BFB_TRY(p.pub.alloc(nwords_pad));
     BFB_TRY(p.q_v.alloc(owned + 1));
     BFB_TRY(p.q_pre.alloc(owned + 1));
-    BFB_TRY(p.q_row.alloc(owned + 1));
     BFB_TRY(p.tile_vstart.alloc(p.tile_cap));
-    const int64_t cblocks = commit_blocks(p.wlo, p.whi) + 1;
-    BFB_TRY(p.block_sums.alloc(2 * cblocks));
+    {
+      const int64_t nunits = (p.whi - (p.wlo & ~(int64_t)31) + 31) / 32 + 1;
+      const int64_t ntiles = (nunits + kScanTile - 1) / kScanTile + 1;
+      BFB_TRY(p.unit_u32.alloc(nunits));
+      BFB_TRY(p.unit_i64.alloc(3 * nunits + 2 * ntiles));
+    }
     BFB_TRY(p.ctr.alloc(1));
     BFB_CUDA(cudaMemset(p.visited.p, 0, nwords_pad * sizeof(uint32_t)));
     BFB_CUDA(cudaMemset(p.start.p, 0, nwords_pad * sizeof(uint32_t)));
@@ -744,6 +832,7 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_CUDA(cudaFuncSetAttribute(k_expand<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
   ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
+  BFB_TRY(set_l2_window(ctx, ctx->parts[0].visited.p, nwords * sizeof(uint32_t)));
   for (auto& ev : D->ev) BFB_CUDA(cudaEventCreate(&ev));
   ctx->engine_ready = true;
   return BFB_OK;
@@ -835,11 +924,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       Part& p = ctx->parts[g];
       PartView v = view_of(ctx, p);
       if (p.whi > p.wlo) {
-        const int64_t cb = commit_blocks(p.wlo, p.whi);
-        k_commit_owned<false><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, off, next_level);
-        k_commit_scan<<<1, 1024, 0, s>>>(v, cb, ctx->run.p);
-        k_commit_owned<true><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, off, next_level);
-        launches += 3;
+        launches += launch_commit(v, off, next_level, ctx->run.p, sms, s);
       }
       if (nwords - (p.whi - p.wlo) > 0) {
         k_commit_rest<<<small_grid, 256, 0, s>>>(v, next_level);
@@ -1001,8 +1086,7 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   BFB_CUDA(cudaMemcpy(&ob[1], ctx->g.offsets.p + p.hi, sizeof(int64_t), cudaMemcpyDeviceToHost));
   p.owned_edges = ob[1] - ob[0];
   const int64_t nwords = (n + 31) / 32;
-  const int64_t nwords_pad = (nwords + kWordsPerCommitBlock - 1) / kWordsPerCommitBlock *
-                                 kWordsPerCommitBlock + kWordsPerCommitBlock;
+  const int64_t nwords_pad = (nwords + kWordPad - 1) / kWordPad * kWordPad + kWordPad;
   BFB_TRY(p.pub.alloc(nwords_pad));
   BFB_TRY(p.pub_alt.alloc(nwords_pad));
   BFB_CUDA(cudaMemset(p.pub.p, 0, nwords_pad * sizeof(uint32_t)));
@@ -1134,11 +1218,7 @@ int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
   k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
   ++D->launches;
   if (p.whi > p.wlo) {
-    const int64_t cb = commit_blocks(p.wlo, p.whi);
-    k_commit_owned<false><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, ctx->g.offsets.p, next_level);
-    k_commit_scan<<<1, 1024, 0, s>>>(v, cb, ctx->run.p);
-    k_commit_owned<true><<<(unsigned)cb, kCommitBlock, 0, s>>>(v, ctx->g.offsets.p, next_level);
-    D->launches += 3;
+    D->launches += launch_commit(v, ctx->g.offsets.p, next_level, ctx->run.p, ctx->num_sms, s);
   }
   if (nwords - (p.whi - p.wlo) > 0) {
     k_commit_rest<<<grid_cap(nwords, 256, ctx->num_sms, 4), 256, 0, s>>>(v, next_level);
