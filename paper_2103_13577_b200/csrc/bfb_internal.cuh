@@ -172,6 +172,7 @@ struct Part {
   DevBuf<uint32_t> pub_alt;        // odd-round snapshot (multi-process mode)
   DevBuf<uint32_t> q_v;            // q_local vertex ids, ascending
   DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local
+  DevBuf<int64_t> q_base;          // offsets[v] - q_pre (adjacency base per row)
   DevBuf<uint32_t> tile_vstart;    // q_local index owning edge t*TILE
   DevBuf<uint32_t> unit_u32;       // commit: owned new vertices per 32-word unit
   DevBuf<int64_t> unit_i64;        // commit: unit degree sums, prefixes, scan tiles

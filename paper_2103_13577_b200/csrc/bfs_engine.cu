@@ -30,9 +30,11 @@ namespace bfb {
 namespace {
 
 constexpr int kExpandBlock = 256;
-constexpr int kExpandItems = 8;
+#ifndef BFB_EXPAND_ITEMS
+#define BFB_EXPAND_ITEMS 8
+#endif
+constexpr int kExpandItems = BFB_EXPAND_ITEMS;
 constexpr int64_t kTile = (int64_t)kExpandBlock * kExpandItems;  // edges per tile
-constexpr int kCommitBlock = 256;
 constexpr int kScanItems = 16;                 // commit unit scan: units per thread
 constexpr int64_t kScanTile = 256 * kScanItems;
 constexpr int64_t kWordPad = 1024;  // bitmap allocation padding (words)
@@ -47,6 +49,7 @@ struct PartView {
   uint32_t* pub;
   uint32_t* q_v;
   int64_t* q_pre;
+  int64_t* q_base;  // offsets[v] - q_pre: adjacency index = q_base + edge prefix
   uint32_t* tile_vstart;
   int64_t abase, nunits;  // commit units: words [abase, abase + 32 * nunits)
   uint32_t* ucnt;
@@ -69,6 +72,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.pub = p.pub.p;
   v.q_v = p.q_v.p;
   v.q_pre = p.q_pre.p;
+  v.q_base = p.q_base.p;
   v.tile_vstart = p.tile_vstart.p;
   v.abase = p.wlo & ~(int64_t)31;
   v.nunits = p.whi > p.wlo ? (p.whi - v.abase + 31) / 32 : 0;
@@ -99,6 +103,7 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
       int64_t d = off[root + 1] - off[root];
       v.q_v[0] = (uint32_t)root;
       v.q_pre[0] = 0;
+      v.q_base[0] = off[root];
       c.q_count = 1;
       c.q_edges = d;
       atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)d);
@@ -166,6 +171,9 @@ __global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartV
   const int64_t ntiles = (T + kTile - 1) / kTile;
   uint32_t* __restrict__ visited = v.visited;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t tag = 0;
+  for (int k = threadIdx.x; k < kTile; k += kExpandBlock) s_own[k] = 0;
+  __syncthreads();
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t e0 = t * kTile;
     const int span = (int)min((int64_t)kTile, T - e0);
@@ -186,9 +194,8 @@ __global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartV
         if (k < nseg) {
           const int64_t pre = __ldg(v.q_pre + vs + k);
           rel[k] = (int32_t)max(pre - e0, (int64_t)INT32_MIN);
-          const uint32_t qv = __ldg(v.q_v + vs + k);
-          base[k] = __ldg(v.off + qv) - pre;
-          sv[k] = qv;
+          base[k] = __ldg(v.q_base + vs + k);
+          if (kParents) sv[k] = __ldg(v.q_v + vs + k);
         }
       }
 #pragma unroll
@@ -211,15 +218,17 @@ __global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartV
       claim_batch<kParents>(u, src, ok, visited, v.parent);
       continue;
     }
-    for (int k = threadIdx.x; k < kTile; k += kExpandBlock) s_own[k] = 0;
-    __syncthreads();
+    // Owner map: row starts scattered with a per-tile tag in the high bits,
+    // so the block max-scan ignores entries left by earlier tiles (no reset).
+    ++tag;
+    const int32_t tg = tag << 12;
+    if (threadIdx.x == 0) s_own[0] = tg;
     for (int k = threadIdx.x; k < nseg; k += kExpandBlock) {
       const int64_t pre = v.q_pre[vs + k];
-      const uint32_t qv = v.q_v[vs + k];
-      s_base[k] = __ldg(v.off + qv) - pre;
-      if (kParents) s_v[k] = qv;
+      s_base[k] = v.q_base[vs + k];
+      if (kParents) s_v[k] = v.q_v[vs + k];
       const int64_t r = pre - e0;
-      if (r > 0 && r < span) s_own[r] = k;
+      if (r > 0 && r < span) s_own[r] = tg | k;
     }
     __syncthreads();
     {  // inclusive max-scan of the owner map, kTile / kExpandBlock entries per thread
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartV
       const int32_t up = __shfl_up_sync(0xffffffffu, inc, 1);
       const int32_t prev = max(carry, lane > 0 ? up : 0);
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) s_own[threadIdx.x * kPer + i] = max(prev, loc[i]);
+      for (int i = 0; i < kPer; ++i) s_own[threadIdx.x * kPer + i] = max(prev, loc[i]) & 0xFFF;
       __syncthreads();
     }
 #pragma unroll
@@ -482,18 +491,29 @@ __global__ void __launch_bounds__(256) k_unit_scan_apply(PartView v) {
   }
 }
 
+// Write pass.  Lane = word computes each word's (count, degree) prefix inside
+// the unit; the stores then run lane = bit, kCommitBatch words at a time, so
+// level / q_v / q_pre / q_base stores are coalesced and the batch's offsets
+// loads are all in flight together (the words are independent once their
+// prefixes are known).
+#ifndef BFB_COMMIT_BATCH
+#define BFB_COMMIT_BATCH 4
+#endif
+constexpr int kCommitBatch = BFB_COMMIT_BATCH;
+
 __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
                                                       uint32_t next_level) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   for (int64_t unit = gw; unit < v.nunits; unit += nw) {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
-    if (!__any_sync(0xffffffffu, nb != 0)) continue;
-    const int64_t w = v.abase + unit * 32 + lane;
-    const int64_t vbase = w << 5;
-    const int64_t dsum = own ? word_degree_sum(own, vbase, off) : 0;
+    const unsigned m = __ballot_sync(0xffffffffu, nb != 0);
+    if (!m) continue;
+    const int64_t w0 = v.abase + unit * 32;
+    const int64_t dsum = own ? word_degree_sum(own, (w0 + lane) << 5, off) : 0;
     const int cnt = __popc(own);
     int cinc = cnt;
 #pragma unroll
@@ -501,27 +521,47 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
       const int t = __shfl_up_sync(0xffffffffu, cinc, dd);
       if (lane >= dd) cinc += t;
     }
-    const int64_t dinc = warp_inclusive_i64(dsum);
-    int64_t pos = v.upos[unit] + (cinc - cnt);
-    int64_t epre = v.uepre[unit] + (dinc - dsum);
-    uint32_t x = nb;
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      const int64_t u = vbase + b;
-      v.level[u] = next_level;
-      if ((own >> b) & 1u) {
-        const int64_t r0 = __ldg(off + u);
-        const int64_t d = __ldg(off + u + 1) - r0;
-        v.q_v[pos] = (uint32_t)u;
-        v.q_pre[pos] = epre;
-        for (int64_t t = (epre + kTile - 1) / kTile; t * kTile < epre + d; ++t)
-          v.tile_vstart[t] = (uint32_t)pos;
-        ++pos;
-        epre += d;
+    const int64_t dinc_w = warp_inclusive_i64(dsum);
+    const int64_t wpos = v.upos[unit] + (cinc - cnt);      // this lane's word: first position
+    const int64_t wepre = v.uepre[unit] + (dinc_w - dsum);  // ... and first edge prefix
+#pragma unroll 1
+    for (int g = 0; g < 32; g += kCommitBatch) {
+      if (!((m >> g) & ((1u << kCommitBatch) - 1u))) continue;
+      uint32_t x[kCommitBatch], xo[kCommitBatch];
+      int64_t r0[kCommitBatch], d[kCommitBatch];
+#pragma unroll
+      for (int k = 0; k < kCommitBatch; ++k) {
+        x[k] = __shfl_sync(0xffffffffu, nb, g + k);
+        xo[k] = __shfl_sync(0xffffffffu, own, g + k);
+        const int64_t u = ((w0 + g + k) << 5) + lane;
+        r0[k] = 0;
+        d[k] = 0;
+        if ((xo[k] >> lane) & 1u) {
+          r0[k] = __ldg(off + u);
+          d[k] = __ldg(off + u + 1) - r0[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kCommitBatch; ++k) {
+        const int64_t u = ((w0 + g + k) << 5) + lane;
+        if ((x[k] >> lane) & 1u) v.level[u] = next_level;
+        const int64_t p0 = __shfl_sync(0xffffffffu, wpos, g + k);
+        const int64_t e0 = __shfl_sync(0xffffffffu, wepre, g + k);
+        if (xo[k]) {
+          const int64_t dinc = warp_inclusive_i64(d[k]);
+          if ((xo[k] >> lane) & 1u) {
+            const int64_t p = p0 + __popc(xo[k] & lt);
+            const int64_t e = e0 + dinc - d[k];
+            v.q_v[p] = (uint32_t)u;
+            v.q_pre[p] = e;
+            v.q_base[p] = r0[k] - e;
+            for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d[k]; ++t)
+              v.tile_vstart[t] = (uint32_t)p;
+          }
+        }
       }
     }
-    if (nb) v.start[w] = a;
+    if (nb) v.start[w0 + lane] = a;
   }
 }
 
@@ -760,6 +800,7 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     if (parts > 1) BFB_TRY(p.pub.alloc(nwords_pad));
     BFB_TRY(p.q_v.alloc(owned + 1));
     BFB_TRY(p.q_pre.alloc(owned + 1));
+    BFB_TRY(p.q_base.alloc(owned + 1));
     BFB_TRY(p.tile_vstart.alloc(p.tile_cap));
     {
       const int64_t nunits = (p.whi - (p.wlo & ~(int64_t)31) + 31) / 32 + 1;
