@@ -58,6 +58,8 @@ typedef struct bfb_run_stats {
   double commit_ms;                  /* level commit / frontier build (timing mode)   */
   int64_t expand_launches;           /* expand kernel launches in this run            */
   int64_t kernel_launches;           /* all kernels this library launched in the run  */
+  int64_t edges_examined;            /* bottom-up levels: edges actually checked      */
+  int64_t bottom_up_levels;          /* levels whose phase 1 ran bottom-up            */
 } bfb_run_stats;
 
 /* ---- library ---------------------------------------------------------- */
@@ -87,6 +89,12 @@ int bfb_create(bfb_ctx** ctx_out, int device);
 void bfb_destroy(bfb_ctx* ctx);
 /* Record per-phase CUDA events inside bfb_bfs (fills *_ms of bfb_run_stats). */
 int bfb_set_timing(bfb_ctx* ctx, int enabled);
+/* Phase-1 direction (paper contribution 3; SPEC.md:172 keeps
+ * the slot): 0 = top-down (Alg. 2, default), 1 = direction-optimizing with
+ * Beamer's switch (TD->BU when frontier edges > unexplored edges / alpha,
+ * BU->TD when frontier < |V| / beta), 2 = bottom-up after the root level.
+ * Levels and RunStats are identical in all modes.  Applies from the next bfb_bfs. */
+int bfb_set_direction(bfb_ctx* ctx, int mode, double alpha, double beta);
 /* Device-side bracket timer on the context's stream: start records a CUDA
  * event, stop records another, synchronizes and returns the elapsed ms. */
 int bfb_timer_start(bfb_ctx* ctx);

@@ -24,6 +24,8 @@ ERR_SELF_EDGE, ERR_DUPLICATE, ERR_NO_REVERSE, ERR_RANGE = -5, -6, -7, -8
 ERR_STATE, ERR_CAPACITY, ERR_CUDA, ERR_OOM = -9, -10, -20, -21
 
 STRATEGY = {"butterfly": 0, "all2all": 1, "all-to-all": 1, "all_to_all": 1}
+DIRECTION = {"top-down": 0, "topdown": 0, "optimizing": 1, "direction-optimizing": 1,
+             "bottom-up": 2}
 
 
 class RunStatsC(ctypes.Structure):
@@ -42,6 +44,8 @@ class RunStatsC(ctypes.Structure):
         ("commit_ms", c_double),
         ("expand_launches", c_int64),
         ("kernel_launches", c_int64),
+        ("edges_examined", c_int64),
+        ("bottom_up_levels", c_int64),
     ]
 
 
@@ -64,6 +68,7 @@ _SIGNATURES = {
     "bfb_create": (c_int, [POINTER(c_void_p), c_int]),
     "bfb_destroy": (None, [c_void_p]),
     "bfb_set_timing": (c_int, [c_void_p, c_int]),
+    "bfb_set_direction": (c_int, [c_void_p, c_int, c_double, c_double]),
     "bfb_timer_start": (c_int, [c_void_p]),
     "bfb_timer_stop": (c_int, [c_void_p, POINTER(c_double)]),
     "bfb_rmat_edges": (c_int, [c_void_p, c_int, c_int64, _U64P, _U64P, _U64P, _U32P]),

@@ -1,0 +1,197 @@
+"""cli module over the B200 engine.
+
+    python -m paper_2103_13577_b200.cli bench    --kronecker 20 8 1 --nodes 4 --fanout 2
+    python -m paper_2103_13577_b200.cli verify   --kronecker 16 8 1 --nodes 9 --fanout 1
+    python -m paper_2103_13577_b200.cli schedule --nodes 16 --fanout 4
+    python -m paper_2103_13577_b200.cli generate --kronecker 4 2 1 --out g.txt
+
+bench follows SPEC.md:389-397: ``roots`` distinct roots sampled uniformly over
+all vertices with ``seed``, one engine run per root, runs sorted by
+time with ``trim`` fastest and slowest dropped, trimmed mean time, teps_nominal
+= |E| / mean and teps_touched = traversed edges / mean, JSON on
+stdout and optional per-run CSV.  verify runs
+the CN-node engine and the single-node engine (the bfs_top_down degenerate
+case) per root and compares full distance arrays, plus the device
+certificate of SPEC.md:130-132; exit status 1 with (root, vertex, expected,
+got) on the first mismatch.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import sys
+
+import numpy as np
+
+from . import engine, graphs, schedule
+
+
+def _load_graph(args):
+    if args.kronecker:
+        s, ef, seed = args.kronecker
+        g = graphs.kronecker(int(s), int(ef), int(seed))
+        return g, f"kronecker-s{s}-ef{ef}-seed{seed}"
+    if not args.graph:
+        raise SystemExit("need --graph PATH or --kronecker SCALE EF SEED")
+    el = load_edge_list(args.graph, args.format)
+    g = graphs.build_csr(graphs.symmetrize(el))
+    return g, args.graph
+
+
+def load_edge_list(path, fmt="edges"):
+    """Minimal reader for the two SPEC formats; the
+    reference's full parser (graphs.py:96-202) is out of this path's scope."""
+    rows, n_decl = [], None
+    with open(path, "rt", encoding="ascii", errors="replace") as fh:
+        if fmt == "mtx":
+            header = fh.readline().strip().lower().split()
+            if len(header) < 4 or header[0] != "%%matrixmarket":
+                raise ValueError("expected '%%MatrixMarket matrix coordinate' header")
+        for line in fh:
+            t = line.strip()
+            if not t or t[0] in "#%":
+                continue
+            parts = t.split()
+            if fmt == "mtx" and n_decl is None:
+                n_decl = max(int(parts[0]), int(parts[1]))
+                continue
+            rows.append((int(parts[0]) - (fmt == "mtx"), int(parts[1]) - (fmt == "mtx")))
+    e = np.asarray(rows, dtype=np.int64).reshape(-1, 2)
+    n = n_decl if n_decl is not None else (int(e.max()) + 1 if e.size else 0)
+    return graphs.EdgeList(e.astype(np.uint32), n)
+
+
+def sample_roots(n, count, seed):
+    """Distinct roots uniform over all vertices; the same set
+    for every (CN, fanout) configuration."""
+    k = min(int(count), int(n))
+    return np.random.default_rng(seed).choice(n, k, replace=False), k < int(count)
+
+
+def cmd_bench(args):
+    g, name = _load_graph(args)
+    p = graphs.partition_1d(g, args.nodes)
+    cfg = engine.EngineConfig(fanout=args.fanout, strategy=args.strategy)
+    roots, short = sample_roots(g.num_vertices, args.roots, args.seed)
+    if len(roots) <= 2 * args.trim:
+        raise SystemExit("roots must exceed 2 * trim")
+    runs = []
+    for r in roots:
+        _, st = engine.run(g, p, int(r), cfg)
+        runs.append({"root": int(r), "elapsed_s": st.elapsed, "levels": st.levels,
+                     "remote_messages": st.remote_messages,
+                     "remote_vertices": st.remote_vertices_transferred,
+                     "buffer_high_water_max": max(st.buffer_high_water),
+                     "traversed_edges": st.traversed_edges,
+                     "rounds_executed": st.rounds_executed,
+                     "frontier_sizes": st.per_level_frontier_size})
+    kept = sorted(runs, key=lambda x: x["elapsed_s"])
+    kept = kept[args.trim:len(kept) - args.trim] if args.trim else kept
+    mean_t = float(np.mean([x["elapsed_s"] for x in kept]))
+    mean_trav = float(np.mean([x["traversed_edges"] for x in kept]))
+    report = {
+        "graph_name": name, "num_vertices": g.num_vertices, "num_edges": g.num_edges,
+        "config": {"nodes": args.nodes, "fanout": args.fanout, "strategy": args.strategy},
+        "roots_sampled": len(runs), "roots_kept": len(kept), "roots_short": bool(short),
+        "mean_time": mean_t, "teps_nominal": g.num_edges / mean_t,
+        "teps_touched": mean_trav / mean_t, "per_run": runs,
+    }
+    print(json.dumps(report))
+    if args.csv:
+        cols = ["root", "elapsed_s", "levels", "remote_messages", "remote_vertices",
+                "buffer_high_water_max"]
+        with open(args.csv, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(cols)
+            for x in runs:
+                w.writerow([x[c] for c in cols])
+    return 0
+
+
+def cmd_verify(args):
+    g, _ = _load_graph(args)
+    p = graphs.partition_1d(g, args.nodes)
+    p1 = graphs.partition_1d(g, 1)
+    roots, _ = sample_roots(g.num_vertices, args.roots, args.seed)
+    cfg = engine.EngineConfig(fanout=args.fanout, strategy=args.strategy)
+    for r in roots:
+        r = int(r)
+        ref, _ = engine.run(g, p1, r)
+        got, _ = engine.run(g, p, r, cfg)
+        bad = np.flatnonzero(ref.d != got.d)
+        if bad.size:
+            v = int(bad[0])
+            print(json.dumps({"ok": False, "root": r, "vertex": v, "expected": int(ref.d[v]),
+                              "got": int(got.d[v])}))
+            return 1
+        cert = g.device.validate(r) if getattr(g, "device", None) is not None else 0
+        if cert:
+            print(json.dumps({"ok": False, "root": r, "certificate_errors": int(cert)}))
+            return 1
+    print(json.dumps({"ok": True, "roots": len(roots), "nodes": args.nodes,
+                      "fanout": args.fanout}))
+    return 0
+
+
+def cmd_schedule(args):
+    s = schedule.make_schedule(args.nodes, args.fanout)
+    print(json.dumps({
+        "num_nodes": args.nodes, "fanout": args.fanout,
+        "rounds": [[list(srcs) for srcs in rnd] for rnd in s],
+        "num_rounds": schedule.num_rounds(args.nodes, args.fanout),
+        "message_count_paper": schedule.message_count_paper(args.nodes, args.fanout),
+        "message_count_remote": schedule.message_count_remote(s),
+    }))
+    return 0
+
+
+def cmd_generate(args):
+    s, ef, seed = args.kronecker
+    g = graphs.kronecker(int(s), int(ef), int(seed))
+    e = g.device.edges()
+    np.savetxt(args.out, e, fmt="%d")
+    print(json.dumps({"num_vertices": g.num_vertices, "num_edges": g.num_edges, "out": args.out}))
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(prog="bflybfs-b200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+
+    def graph_args(sp):
+        sp.add_argument("--graph")
+        sp.add_argument("--format", default="edges", choices=["edges", "mtx"])
+        sp.add_argument("--kronecker", nargs=3, type=int, metavar=("SCALE", "EF", "SEED"))
+
+    b = sub.add_parser("bench")
+    graph_args(b)
+    b.add_argument("--nodes", type=int, default=1)
+    b.add_argument("--fanout", type=int, default=1)
+    b.add_argument("--strategy", default="butterfly", choices=["butterfly", "all2all"])
+    b.add_argument("--roots", type=int, default=100)
+    b.add_argument("--trim", type=int, default=25)
+    b.add_argument("--seed", type=int, default=0)
+    b.add_argument("--csv")
+    v = sub.add_parser("verify")
+    graph_args(v)
+    v.add_argument("--nodes", type=int, default=1)
+    v.add_argument("--fanout", type=int, default=1)
+    v.add_argument("--strategy", default="butterfly", choices=["butterfly", "all2all"])
+    v.add_argument("--roots", type=int, default=20)
+    v.add_argument("--seed", type=int, default=0)
+    sc = sub.add_parser("schedule")
+    sc.add_argument("--nodes", type=int, required=True)
+    sc.add_argument("--fanout", type=int, required=True)
+    gen = sub.add_parser("generate")
+    gen.add_argument("--kronecker", nargs=3, type=int, required=True,
+                     metavar=("SCALE", "EF", "SEED"))
+    gen.add_argument("--out", required=True)
+    args = ap.parse_args(argv)
+    return {"bench": cmd_bench, "verify": cmd_verify, "schedule": cmd_schedule,
+            "generate": cmd_generate}[args.cmd](args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

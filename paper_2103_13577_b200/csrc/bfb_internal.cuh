@@ -151,6 +151,7 @@ struct PartCounters {
 
 // Device-resident run statistics (RunStats).
 struct RunCounters {
+  int64_t edges_examined;  // bottom-up levels: edges actually checked
   int64_t remote_messages;
   int64_t remote_vertices;
   int64_t traversed_edges;
@@ -170,6 +171,7 @@ struct Part {
   DevBuf<uint32_t> parent;         // phase-1 parents (n) when wanted
   DevBuf<uint32_t> pub;            // published round snapshot (n bits)
   DevBuf<uint32_t> pub_alt;        // odd-round snapshot (multi-process mode)
+  DevBuf<uint32_t> front;          // level-L frontier bitmap (bottom-up phase 1)
   DevBuf<uint32_t> q_v;            // q_local vertex ids, ascending
   DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local
   DevBuf<int64_t> q_base;          // offsets[v] - q_pre (adjacency base per row)
@@ -203,6 +205,8 @@ struct bfb_ctx {
   bfb::EngineTables* tables = nullptr;
   int expand_grid = 0;
   bool timing = false;
+  int direction = 0;                  // 0 top-down, 1 direction-optimizing, 2 bottom-up
+  double do_alpha = 14.0, do_beta = 24.0;
   bool have_run = false;
   int64_t last_root = -1;
   int64_t last_levels = 0;

@@ -47,6 +47,7 @@ struct PartView {
   uint32_t* level;
   uint32_t* parent;
   uint32_t* pub;
+  uint32_t* front;  // level-L frontier bitmap, written at commit when direction != 0
   uint32_t* q_v;
   int64_t* q_pre;
   int64_t* q_base;  // offsets[v] - q_pre: adjacency index = q_base + edge prefix
@@ -70,6 +71,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.level = p.level.p;
   v.parent = p.parent.p;
   v.pub = p.pub.p;
+  v.front = ctx->direction ? p.front.p : nullptr;
   v.q_v = p.q_v.p;
   v.q_pre = p.q_pre.p;
   v.q_base = p.q_base.p;
@@ -96,6 +98,7 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
   if (threadIdx.x == 0) {
     v.visited[w] = b;
     v.start[w] = b;
+    if (v.front) v.front[w] = b;
     v.level[root] = 0;
     if (v.parent) v.parent[root] = (uint32_t)root;
     PartCounters c{};
@@ -561,7 +564,10 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
         }
       }
     }
-    if (nb) v.start[w0 + lane] = a;
+    if (nb) {
+      v.start[w0 + lane] = a;
+      if (v.front) v.front[w0 + lane] = nb;
+    }
   }
 }
 
@@ -572,20 +578,77 @@ __global__ void k_commit_rest(PartView v, uint32_t next_level) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t w = i < v.wlo ? i : i + (v.whi - v.wlo);
     const uint32_t a = v.visited[w];
-    uint32_t x = a & ~v.start[w];
-    if (!x) continue;
-    fr += __popc(x);
+    const uint32_t nbits = a & ~v.start[w];
+    if (!nbits) continue;
+    fr += __popc(nbits);
     const int64_t vb = w << 5;
+    uint32_t x = nbits;
     while (x) {
       const int b = __ffs(x) - 1;
       x &= x - 1;
       v.level[vb + b] = next_level;
     }
     v.start[w] = a;
+    if (v.front) v.front[w] = nbits;
   }
   __shared__ int64_t red[32];
   fr = block_sum_i64(fr, red);
   if (threadIdx.x == 0 && fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+}
+
+// ------------------------------------------------------- bottom-up phase 1 --
+// Direction-optimizing phase 1 (Beamer et al.): every owned
+// unvisited vertex scans its row (ascending ids, so hubs first) for a
+// neighbour in the level-L frontier bitmap and claims itself on the first hit.
+// Discoveries are owned vertices only; phase 2 and the commit are unchanged,
+// so levels, frontier sizes and the exchange accounting are identical to
+// top-down.  Warp = one bitmap word (32 consecutive vertices); each lane
+// checks kBuBatch neighbours per round trip.
+constexpr int kBuBatch = 4;
+
+template <bool kParents>
+__global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* __restrict__ adj,
+                                                   unsigned long long* examined) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t* __restrict__ front = v.front;
+  unsigned long long ex = 0;
+  for (int64_t w = v.wlo + gw; w < v.whi; w += nw) {
+    const uint32_t vis = v.visited[w];
+    const uint32_t cand = owned_mask(w, v.lo, v.hi) & ~vis;
+    if (!cand) continue;
+    const int64_t u = (w << 5) + lane;
+    bool found = false;
+    uint32_t par = 0;
+    if ((cand >> lane) & 1u) {
+      const int64_t b = __ldg(v.off + u), e = __ldg(v.off + u + 1);
+      for (int64_t j = b; j < e && !found; j += kBuBatch) {
+        uint32_t p[kBuBatch];
+        bool hit[kBuBatch];
+#pragma unroll
+        for (int k = 0; k < kBuBatch; ++k) p[k] = j + k < e ? ld_stream_u32(adj + j + k) : 0u;
+#pragma unroll
+        for (int k = 0; k < kBuBatch; ++k)
+          hit[k] = j + k < e && ((front[p[k] >> 5] >> (p[k] & 31)) & 1u);
+#pragma unroll
+        for (int k = 0; k < kBuBatch; ++k) {
+          if (!found && j + k < e) {
+            ++ex;
+            if (hit[k]) {
+              found = true;
+              par = p[k];
+            }
+          }
+        }
+      }
+    }
+    const uint32_t nbits = __ballot_sync(0xffffffffu, found);
+    if (lane == 0 && nbits) v.visited[w] = vis | nbits;  // this node is the word's only writer
+    if (kParents && found) v.parent[u] = par;
+  }
+  ex = (unsigned long long)warp_sum_i64((int64_t)ex);
+  if (lane == 0 && ex) atomicAdd(examined, ex);
 }
 
 // ------------------------------------------------------------ outputs ----
@@ -802,6 +865,7 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_TRY(p.q_pre.alloc(owned + 1));
     BFB_TRY(p.q_base.alloc(owned + 1));
     BFB_TRY(p.tile_vstart.alloc(p.tile_cap));
+    BFB_TRY(p.front.alloc(nwords_pad));
     {
       const int64_t nunits = (p.whi - (p.wlo & ~(int64_t)31) + 31) / 32 + 1;
       const int64_t ntiles = (nunits + kScanTile - 1) / kScanTile + 1;
@@ -909,9 +973,16 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
     BFB_CUDA(cudaMemsetAsync(p.level.p, 0xFF, n * sizeof(uint32_t), s));
     if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
+    if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
     k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), off, root, g == owner ? 1 : 0, ctx->run.p);
     ++launches;
   }
+  // Direction-optimizing state (Beamer's heuristic): switch to bottom-up when
+  // the frontier's edges exceed the unexplored edges / alpha, back to
+  // top-down when the frontier shrinks below |V| / beta.
+  bool bottom_up = ctx->direction == 2;
+  int64_t bu_levels = 0;
+  int64_t prev_frontier = 1;
   const int64_t bytes_per_transfer = nwords * (int64_t)sizeof(uint32_t);
   int64_t level = 0;
   int64_t nsizes = 0;
@@ -925,13 +996,22 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     // Phase 1
     for (int g = 0; g < P; ++g) {
       PartView v = view_of(ctx, ctx->parts[g]);
-      if (ctx->want_parents)
+      if (bottom_up) {
+        const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo) * 32, 256, sms, 8);
+        unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
+        if (ctx->want_parents)
+          k_bottom_up<true><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+        else
+          k_bottom_up<false><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+      } else if (ctx->want_parents) {
         k_expand<true><<<ctx->expand_grid, kExpandBlock, 0, s>>>(v, ctx->g.adj.p);
-      else
+      } else {
         k_expand<false><<<ctx->expand_grid, kExpandBlock, 0, s>>>(v, ctx->g.adj.p);
+      }
       ++launches;
       ++expand_launches;
     }
+    if (bottom_up) ++bu_levels;
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[3], s));
     // Phase 2
     if (!D->rounds.empty()) {
@@ -961,6 +1041,9 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     k_commit_prep<<<1, 256, 0, s>>>(D->ctrs.p, P);
     ++launches;
     const uint32_t next_level = (uint32_t)(level + 1);
+    if (ctx->direction)
+      for (int g = 0; g < P; ++g)
+        BFB_CUDA(cudaMemsetAsync(ctx->parts[g].front.p, 0, nwords * sizeof(uint32_t), s));
     for (int g = 0; g < P; ++g) {
       Part& p = ctx->parts[g];
       PartView v = view_of(ctx, p);
@@ -973,9 +1056,18 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       }
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
-    // Termination: node 0's synchronized frontier.
+    // Termination: node 0's synchronized frontier.  With
+    // direction optimization also every node's next-frontier edge count and
+    // the degree sum of everything visited so far.
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned, &ctx->parts[0].ctr.p->frontier, sizeof(int64_t),
                              cudaMemcpyDeviceToHost, s));
+    if (ctx->direction == 1) {
+      for (int g = 0; g < P; ++g)
+        BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 2 + g, &ctx->parts[g].ctr.p->q_edges,
+                                 sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 1, &ctx->run.p->traversed_edges, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
+    }
     BFB_CUDA(cudaStreamSynchronize(s));
     BFB_CUDA(cudaGetLastError());
     if (ctx->timing) {
@@ -989,6 +1081,19 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     }
     const int64_t frontier = ctx->pinned[0];
     if (frontier == 0) break;
+    if (ctx->direction == 1) {
+      int64_t mf = 0;
+      for (int g = 0; g < P; ++g) mf += ctx->pinned[2 + g];
+      const int64_t explored = ctx->pinned[1];  // degrees of all visited vertices
+      const double mu = (double)(ctx->g.m - explored);
+      if (!bottom_up && (double)mf > mu / ctx->do_alpha && frontier > prev_frontier) {
+        bottom_up = true;
+      } else if (bottom_up && (double)frontier < (double)n / ctx->do_beta &&
+                 frontier < prev_frontier) {
+        bottom_up = false;
+      }
+    }
+    prev_frontier = frontier;
     if (nsizes < max_levels && sizes_out) sizes_out[nsizes] = frontier;
     ctx->last_sizes.push_back(frontier);
     ++nsizes;
@@ -1048,6 +1153,8 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     st->commit_ms = t_commit;
     st->expand_launches = expand_launches;
     st->kernel_launches = launches;
+    st->edges_examined = rc.edges_examined;
+    st->bottom_up_levels = bu_levels;
   }
   // buffer-bound check: incoming <= f * |V|
   for (auto x : hw)

@@ -191,6 +191,16 @@ int bfb_set_timing(bfb_ctx* ctx, int enabled) {
   return BFB_OK;
 }
 
+int bfb_set_direction(bfb_ctx* ctx, int mode, double alpha, double beta) {
+  CTX_GUARD(ctx);
+  if (mode < 0 || mode > 2 || !(alpha > 0) || !(beta > 0))
+    return fail(BFB_ERR_INVALID, "bad direction parameters");
+  ctx->direction = mode;
+  ctx->do_alpha = alpha;
+  ctx->do_beta = beta;
+  return BFB_OK;
+}
+
 int bfb_timer_start(bfb_ctx* ctx) {
   CTX_GUARD(ctx);
   if (!ctx->timer[0]) {

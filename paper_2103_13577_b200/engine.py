@@ -23,13 +23,18 @@ from .graphs import UNREACHED, device_graph
 class EngineConfig:
     """SPEC.md:279-282.  ``worker_mode`` and ``intra_node_parallelism`` are
     accepted for API compatibility: device results are deterministic in both
-    modes.  ``parents`` additionally returns BFS parents."""
+    modes.  ``parents`` additionally returns BFS parents.  ``direction``
+    selects phase 1: "top-down" (Alg. 2, the reference semantics) or
+    "optimizing" (top-down/bottom-up switching, the paper's contribution 3,
+    PAPER.md:54; SPEC.md:172 keeps the slot) -- levels, frontier sizes and the
+    exchange accounting are identical either way."""
 
     fanout: int = 1
     strategy: str = "butterfly"
     worker_mode: str = "lockstep"
     intra_node_parallelism: int = 1
     parents: bool = False
+    direction: str = "top-down"
 
     def __post_init__(self):
         if self.intra_node_parallelism < 1:
@@ -38,6 +43,8 @@ class EngineConfig:
             raise ValueError(f"unknown worker_mode {self.worker_mode!r}")
         if self.strategy not in _lib.STRATEGY:
             raise ValueError(f"unknown strategy {self.strategy!r}")
+        if self.direction not in _lib.DIRECTION:
+            raise ValueError(f"unknown direction {self.direction!r}")
 
 
 @dataclass
@@ -65,6 +72,8 @@ class RunStats:
     exchange_bytes: int = 0
     device_ms: dict = field(default_factory=dict)
     kernel_launches: int = 0
+    edges_examined: int = 0
+    bottom_up_levels: int = 0
 
 
 def _check_partition(g, p):
@@ -87,6 +96,7 @@ def run(g, p, root, cfg=None):
         raise ValueError("fanout exceeds num_nodes")
     dg = device_graph(g)
     dg.setup(b, cfg.fanout, cfg.strategy, parents=cfg.parents)
+    dg.set_direction(cfg.direction)
     lv, pa, sizes, st, hw = dg.bfs(root, levels=True, parents=cfg.parents)
     return DistanceArray(lv, root, pa), stats_of(sizes, st, hw)
 
@@ -106,13 +116,16 @@ def stats_of(sizes, st, hw):
         device_ms={"total": st.elapsed_ms, "expand": st.expand_ms,
                    "exchange": st.exchange_ms, "commit": st.commit_ms},
         kernel_launches=int(st.kernel_launches),
+        edges_examined=int(st.edges_examined),
+        bottom_up_levels=int(st.bottom_up_levels),
     )
 
 
 def all_to_all_sync_config(cfg):
     """EngineConfig for the all-to-all strategy."""
     return EngineConfig(fanout=cfg.fanout, strategy="all2all", worker_mode=cfg.worker_mode,
-                        intra_node_parallelism=cfg.intra_node_parallelism, parents=cfg.parents)
+                        intra_node_parallelism=cfg.intra_node_parallelism, parents=cfg.parents,
+                        direction=cfg.direction)
 
 
 __all__ = ["EngineConfig", "DistanceArray", "RunStats", "run", "UNREACHED"]

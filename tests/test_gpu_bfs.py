@@ -123,6 +123,41 @@ def test_acceptance_sweep_vs_oracle_engine(cn):
                     assert not ov.check_parents(off, adj, r, d.d, d.parents)
 
 
+@pytest.mark.parametrize("direction", ["optimizing", "bottom-up"])
+@pytest.mark.parametrize("cn", [1, 3, 8])
+def test_direction_optimizing_identical_results(direction, cn):
+    """Bottom-up / direction-optimizing phase 1: levels, frontier
+    sizes and every exchange counter identical to the top-down oracle engine."""
+    rng = np.random.default_rng(7 + cn)
+    for name, (off, adj) in _sweep_graphs():
+        n = off.size - 1
+        g = _g(off, adj)
+        p = graphs.partition_1d(g, cn)
+        for r in rng.choice(n, 2, replace=False):
+            r = int(r)
+            f = min(2, cn)
+            d, st = engine.run(g, p, r, engine.EngineConfig(fanout=f, parents=True,
+                                                          direction=direction))
+            assert np.array_equal(d.d, ob.bfs_top_down(off, adj, r)), (name, cn, direction, r)
+            _, ost = oe.run(off, adj, p.boundaries, r, fanout=f)
+            assert _same_stats(st, ost), (name, cn, direction, r)
+            assert not ov.check_parents(off, adj, r, d.d, d.parents)
+            if direction == "bottom-up" and st.levels > 1:
+                assert st.bottom_up_levels == st.levels - 1
+
+
+def test_direction_optimizing_switches_on_kronecker(golden):
+    e = golden["s16_ef8"]
+    g = graphs.kronecker(16, 8, 1)
+    p = graphs.partition_1d(g, 1)
+    for r, want in e["bfs"].items():
+        d, st = engine.run(g, p, int(r), engine.EngineConfig(direction="optimizing", parents=True))
+        assert sha16(d.d) == want["levels_sha"]
+        assert st.traversed_edges == want["traversed_edges"]
+        if len(want["sizes"]) > 3:
+            assert st.bottom_up_levels >= 1 and st.edges_examined < st.traversed_edges
+
+
 def test_all2all_message_reduction_cn16():
     off, adj = util.gnp_graph(3000, 0.01)
     g = _g(off, adj)
