@@ -92,8 +92,10 @@ int bfb_set_timing(bfb_ctx* ctx, int enabled);
 /* Phase-1 direction (paper contribution 3; SPEC.md:172 keeps
  * the slot): 0 = top-down (Alg. 2, default), 1 = direction-optimizing with
  * Beamer's switch (TD->BU when frontier edges > unexplored edges / alpha,
- * BU->TD when frontier < |V| / beta), 2 = bottom-up after the root level.
- * Levels and RunStats are identical in all modes.  Applies from the next bfb_bfs. */
+ * BU->TD when frontier < |V| / beta), 2 = bottom-up at every level (testing).
+ * Levels, frontier sizes and traversed edges are identical in all modes (the
+ * exchange volumes differ: bottom-up discoveries are owned vertices only).
+ * Applies from the next bfb_bfs. */
 int bfb_set_direction(bfb_ctx* ctx, int mode, double alpha, double beta);
 /* Device-side bracket timer on the context's stream: start records a CUDA
  * event, stop records another, synchronizes and returns the elapsed ms. */

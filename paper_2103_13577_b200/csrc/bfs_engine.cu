@@ -571,6 +571,31 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
   }
 }
 
+// Commit without the queue: levels (coalesced, lane = bit), start := visited
+// and the frontier bitmap for the owned words.
+__global__ void __launch_bounds__(256) k_commit_light(PartView v, uint32_t next_level) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t unit = gw; unit < v.nunits; unit += nw) {
+    uint32_t a, nb, own;
+    unit_word(v, unit, lane, a, nb, own);
+    unsigned m = __ballot_sync(0xffffffffu, nb != 0);
+    if (!m) continue;
+    const int64_t w0 = v.abase + unit * 32;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
+      if ((x >> lane) & 1u) v.level[((w0 + j) << 5) + lane] = next_level;
+    }
+    if (nb) {
+      v.start[w0 + lane] = a;
+      if (v.front) v.front[w0 + lane] = nb;
+    }
+  }
+}
+
 __global__ void k_commit_rest(PartView v, uint32_t next_level) {
   int64_t fr = 0;
   const int64_t span = v.nwords - (v.whi - v.wlo);
@@ -601,7 +626,7 @@ __global__ void k_commit_rest(PartView v, uint32_t next_level) {
 // unvisited vertex scans its row (ascending ids, so hubs first) for a
 // neighbour in the level-L frontier bitmap and claims itself on the first hit.
 // Discoveries are owned vertices only; phase 2 and the commit are unchanged,
-// so levels, frontier sizes and the exchange accounting are identical to
+// so levels, frontier sizes and traversed edges are identical to
 // top-down.  Warp = one bitmap word (32 consecutive vertices); each lane
 // checks kBuBatch neighbours per round trip.
 constexpr int kBuBatch = 4;
@@ -739,16 +764,37 @@ __global__ void k_merge_peers(SrcList L, uint32_t* __restrict__ vis, int64_t nwo
 }
 
 // Owned-words commit (count -> pair scan -> write); returns kernels launched.
-int launch_commit(const PartView& v, const int64_t* off, uint32_t next_level, RunCounters* run,
-                  int sms, cudaStream_t s) {
+// First half of the owned-words commit: per-unit counts and degree sums and
+// the tile scan (totals -> ctr->q_count / q_edges, RunStats traversed_edges).
+int launch_commit_count(const PartView& v, const int64_t* off, RunCounters* run, int sms,
+                        cudaStream_t s) {
   const int64_t ntiles = std::max<int64_t>(1, (v.nunits + kScanTile - 1) / kScanTile);
-  const unsigned grid = grid_cap(v.nunits * 32, 256, sms, 8);
-  k_commit_count<<<grid, 256, 0, s>>>(v, off);
+  k_commit_count<<<grid_cap(v.nunits * 32, 256, sms, 8), 256, 0, s>>>(v, off);
   k_unit_scan_reduce<<<(unsigned)ntiles, 256, 0, s>>>(v);
   k_unit_scan_tiles<<<1, 1024, 0, s>>>(v, ntiles, run);
+  return 3;
+}
+
+// Second half: with_queue builds the next q_local (unit prefixes + write);
+// without it (next phase 1 runs bottom-up, which reads only bitmaps) only
+// levels, the start snapshot and the frontier bitmap are written.
+int launch_commit_write(const PartView& v, const int64_t* off, uint32_t next_level, bool with_queue,
+                        int sms, cudaStream_t s) {
+  const int64_t ntiles = std::max<int64_t>(1, (v.nunits + kScanTile - 1) / kScanTile);
+  const unsigned grid = grid_cap(v.nunits * 32, 256, sms, 8);
+  if (!with_queue) {
+    k_commit_light<<<grid, 256, 0, s>>>(v, next_level);
+    return 1;
+  }
   k_unit_scan_apply<<<(unsigned)ntiles, 256, 0, s>>>(v);
   k_commit_write<<<grid, 256, 0, s>>>(v, off, next_level);
-  return 5;
+  return 2;
+}
+
+int launch_commit(const PartView& v, const int64_t* off, uint32_t next_level, RunCounters* run,
+                  int sms, cudaStream_t s) {
+  return launch_commit_count(v, off, run, sms, s) +
+         launch_commit_write(v, off, next_level, true, sms, s);
 }
 
 }  // namespace
@@ -1047,27 +1093,47 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     for (int g = 0; g < P; ++g) {
       Part& p = ctx->parts[g];
       PartView v = view_of(ctx, p);
-      if (p.whi > p.wlo) {
-        launches += launch_commit(v, off, next_level, ctx->run.p, sms, s);
-      }
+      if (p.whi > p.wlo) launches += launch_commit_count(v, off, ctx->run.p, sms, s);
       if (nwords - (p.whi - p.wlo) > 0) {
         k_commit_rest<<<small_grid, 256, 0, s>>>(v, next_level);
         ++launches;
       }
     }
-    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
     // Termination: node 0's synchronized frontier.  With
-    // direction optimization also every node's next-frontier edge count and
-    // the degree sum of everything visited so far.
-    BFB_CUDA(cudaMemcpyAsync(ctx->pinned, &ctx->parts[0].ctr.p->frontier, sizeof(int64_t),
-                             cudaMemcpyDeviceToHost, s));
+    // direction optimization the next phase-1 direction is chosen here, from
+    // every node's next-frontier edge count and the degree sum of everything
+    // visited so far, before the commit's write half (which skips the queue
+    // when phase 1 will run bottom-up).
+    bool next_bu = ctx->direction == 2;
+    int64_t frontier = -1;
     if (ctx->direction == 1) {
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned, &ctx->parts[0].ctr.p->frontier, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
       for (int g = 0; g < P; ++g)
         BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 2 + g, &ctx->parts[g].ctr.p->q_edges,
                                  sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 1, &ctx->run.p->traversed_edges, sizeof(int64_t),
                                cudaMemcpyDeviceToHost, s));
+      BFB_CUDA(cudaStreamSynchronize(s));
+      frontier = ctx->pinned[0];
+      int64_t mf = 0;
+      for (int g = 0; g < P; ++g) mf += ctx->pinned[2 + g];
+      const double mu = (double)(ctx->g.m - ctx->pinned[1]);  // unexplored edges
+      next_bu = bottom_up;
+      if (!bottom_up && (double)mf > mu / ctx->do_alpha && frontier > prev_frontier)
+        next_bu = true;
+      else if (bottom_up && (double)frontier < (double)n / ctx->do_beta && frontier < prev_frontier)
+        next_bu = false;
     }
+    for (int g = 0; g < P; ++g) {
+      Part& p = ctx->parts[g];
+      if (p.whi > p.wlo)
+        launches += launch_commit_write(view_of(ctx, p), off, next_level, !next_bu, sms, s);
+    }
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
+    if (frontier < 0)
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned, &ctx->parts[0].ctr.p->frontier, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaStreamSynchronize(s));
     BFB_CUDA(cudaGetLastError());
     if (ctx->timing) {
@@ -1079,20 +1145,9 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       t_exchange += b;
       t_commit += c;
     }
-    const int64_t frontier = ctx->pinned[0];
+    frontier = ctx->pinned[0];
     if (frontier == 0) break;
-    if (ctx->direction == 1) {
-      int64_t mf = 0;
-      for (int g = 0; g < P; ++g) mf += ctx->pinned[2 + g];
-      const int64_t explored = ctx->pinned[1];  // degrees of all visited vertices
-      const double mu = (double)(ctx->g.m - explored);
-      if (!bottom_up && (double)mf > mu / ctx->do_alpha && frontier > prev_frontier) {
-        bottom_up = true;
-      } else if (bottom_up && (double)frontier < (double)n / ctx->do_beta &&
-                 frontier < prev_frontier) {
-        bottom_up = false;
-      }
-    }
+    bottom_up = next_bu;
     prev_frontier = frontier;
     if (nsizes < max_levels && sizes_out) sizes_out[nsizes] = frontier;
     ctx->last_sizes.push_back(frontier);

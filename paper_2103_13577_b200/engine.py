@@ -27,7 +27,7 @@ class EngineConfig:
     selects phase 1: "top-down" (Alg. 2, the reference semantics) or
     "optimizing" (top-down/bottom-up switching, the paper's contribution 3,
     PAPER.md:54; SPEC.md:172 keeps the slot) -- levels, frontier sizes and the
-    exchange accounting are identical either way."""
+    traversed-edge count are identical either way (exchange volumes differ)."""
 
     fanout: int = 1
     strategy: str = "butterfly"
