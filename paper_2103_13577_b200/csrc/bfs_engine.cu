@@ -121,157 +121,329 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
 }
 
 // ------------------------------------------------------------ phase 1 ----
-// Probe the visited bitmap for each gathered neighbour and claim the unvisited
-// ones (check-and-set).  Without parents a fire-and-forget
-// red.or suffices (the commit pass finds the new bits); with parents the
-// atomic's old value elects one winner per vertex, which writes the parent.
+// Phase 1: edge-balanced top-down expansion of q_local.
+// The frontier's edges are cut into 2048-edge tiles (load-balanced search
+// over the degree prefix q_pre); blocks stride over tiles.  Per edge: the
+// adjacency word, a probe of the visited bitmap and, when the probe finds the
+// bit clear, a fire-and-forget red.or claim (check-and-set) --
+// the commit finds the new bits as visited & ~start, so no claim needs the
+// atomic's old value.
+//
+// Software pipeline, one tile deep: while the probes of tile t are in flight
+// the block stages tile t+grid -- resolves each edge's row (from registers
+// for hub tiles of at most kRegSegs rows, else from a shared-memory owner
+// map) and issues cp.async copies of its adjacency words into the other half
+// of a double-buffered shared ring.  Each thread copies and later reads the
+// same ring slots, so the ring needs no block barrier; the adjacency HBM
+// latency and the row-resolution latency both overlap the probe latency.
+//
+// Parents: every claimant whose probe saw the bit clear stores its row
+// vertex as u's parent (plain store, last writer wins).  Every such writer is
+// a level-L vertex adjacent to u and u is discovered at level L+1 (bits set
+// before the launch are never seen clear), so whichever store lands is a
+// valid BFS parent -- no atomic with return on the critical path.
+constexpr int kRegSegs = 4;
+#ifndef BFB_EXPAND_MINB
+#define BFB_EXPAND_MINB 4
+#endif
+constexpr int kExpandMinBlocks = BFB_EXPAND_MINB;  // 4 blocks, 32 warps per SM
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
+// 4-byte async global -> shared copy; the adjacency is read once per BFS, so
+// it is marked evict-first in L2 (the visited bitmap stays resident).
+__device__ __forceinline__ void cp_async_u32(uint32_t* dst, const uint32_t* src, uint64_t pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 template <bool kParents>
-__device__ __forceinline__ void claim_batch(const uint32_t (&u)[kExpandItems],
-                                            const uint32_t (&src)[kExpandItems], unsigned okmask,
-                                            uint32_t* __restrict__ visited,
-                                            uint32_t* __restrict__ parent) {
-  uint32_t wv[kExpandItems];
+struct ExpandSmem {
+  static constexpr int kP = kParents ? kTile : 1;
+  int64_t base[kTile + 1];       // per row: adjacency index - edge prefix (q_base)
+  uint32_t ring[2][kTile];       // adjacency words of the tile in flight / being staged
+  uint32_t ring_src[2][kP];      // parents: row vertex per edge (thread-private slots)
+  int32_t own[kTile];            // owner map: edge -> row within the tile
+  uint32_t rowv[kP + 1];         // per row: vertex id (parents)
+  int32_t wmax[kExpandBlock / 32];
+};
+
+// Stage tile t into ring slot `slot`: resolve rows, issue the cp.async copies,
+// record row vertices for parents.  Block-uniform (uses __syncthreads on the
+// owner-map path).  Returns the tile's edge count.
+template <bool kParents>
+__device__ __forceinline__ int stage_tile(const PartView& v, const uint32_t* __restrict__ adj,
+                                          ExpandSmem<kParents>& S, int slot, int64_t t, int64_t ntiles,
+                                          int64_t T, int64_t qc, int32_t& tag, uint64_t pol) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t e0 = t * kTile;
+  const int span = (int)min((int64_t)kTile, T - e0);
+  const int64_t vs = v.tile_vstart[t];
+  const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
+  const int nseg = (int)(ve - vs + 1);
+  uint32_t* ring = S.ring[slot];
+  if (nseg <= kRegSegs) {
+    int32_t rel[kRegSegs];
+    int64_t base[kRegSegs];
+    uint32_t sv[kRegSegs];
 #pragma unroll
-  for (int it = 0; it < kExpandItems; ++it)
-    if ((okmask >> it) & 1u) wv[it] = visited[u[it] >> 5];
+    for (int k = 0; k < kRegSegs; ++k) {
+      rel[k] = INT32_MAX;
+      base[k] = 0;
+      sv[k] = 0;
+      if (k < nseg) {
+        const int64_t pre = __ldg(v.q_pre + vs + k);
+        rel[k] = (int32_t)max(pre - e0, (int64_t)INT32_MIN);
+        base[k] = __ldg(v.q_base + vs + k);
+        if (kParents) sv[k] = __ldg(v.q_v + vs + k);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < kExpandItems; ++it) {
+      const int r = it * kExpandBlock + threadIdx.x;
+      if (r < span) {
+        int64_t b = base[0];
+        uint32_t s0 = sv[0];
+#pragma unroll
+        for (int k = 1; k < kRegSegs; ++k)
+          if (r >= rel[k]) {
+            b = base[k];
+            s0 = sv[k];
+          }
+        cp_async_u32(ring + r, adj + b + e0 + r, pol);
+        if (kParents) S.ring_src[slot][r] = s0;
+      }
+    }
+    cp_async_commit();
+    return span;
+  }
+  // Owner map: row starts scattered with a per-tile tag in the high bits, so
+  // the block max-scan ignores entries left by earlier tiles (no reset).
+  __syncthreads();  // every thread is done reading the previous map
+  ++tag;
+  const int32_t tg = tag << 12;
+  if (threadIdx.x == 0) S.own[0] = tg;
+  for (int k = threadIdx.x; k < nseg; k += kExpandBlock) {
+    const int64_t pre = v.q_pre[vs + k];
+    S.base[k] = v.q_base[vs + k];
+    if (kParents) S.rowv[k] = v.q_v[vs + k];
+    const int64_t r = pre - e0;
+    if (r > 0 && r < span) S.own[r] = tg | k;
+  }
+  __syncthreads();
+  {  // inclusive max-scan of the owner map, kTile / kExpandBlock entries per thread
+    constexpr int kPer = kTile / kExpandBlock;
+    int32_t loc[kPer];
+    int32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      run = max(run, S.own[threadIdx.x * kPer + i]);
+      loc[i] = run;
+    }
+    int32_t inc = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc = max(inc, o);
+    }
+    if (lane == 31) S.wmax[warp] = inc;
+    __syncthreads();
+    int32_t carry = 0;
+    for (int w = 0; w < warp; ++w) carry = max(carry, S.wmax[w]);
+    const int32_t up = __shfl_up_sync(0xffffffffu, inc, 1);
+    const int32_t prev = max(carry, lane > 0 ? up : 0);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) S.own[threadIdx.x * kPer + i] = max(prev, loc[i]) & 0xFFF;
+    __syncthreads();
+  }
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
-    if ((okmask >> it) & 1u) {
+    const int r = it * kExpandBlock + threadIdx.x;
+    if (r < span) {
+      const int sg = S.own[r];
+      cp_async_u32(ring + r, adj + S.base[sg] + e0 + r, pol);
+      if (kParents) S.ring_src[slot][r] = S.rowv[sg];
+    }
+  }
+  cp_async_commit();
+  return span;
+}
+
+template <bool kParents>
+__global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartView v,
+                                                         const uint32_t* __restrict__ adj) {
+  extern __shared__ __align__(16) unsigned char expand_smem[];
+  ExpandSmem<kParents>& S = *reinterpret_cast<ExpandSmem<kParents>*>(expand_smem);
+  const int64_t T = v.ctr->q_edges;
+  if (T == 0) return;
+  const int64_t qc = v.ctr->q_count;
+  const int64_t ntiles = (T + kTile - 1) / kTile;
+  int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  uint32_t* __restrict__ visited = v.visited;
+  uint32_t* __restrict__ parent = v.parent;
+  const uint64_t pol = l2_evict_first_policy();
+  int32_t tag = 0;
+  for (int k = threadIdx.x; k < kTile; k += kExpandBlock) S.own[k] = 0;
+  int slot = 0;
+  int span = stage_tile<kParents>(v, adj, S, 0, t, ntiles, T, qc, tag, pol);
+  for (; t < ntiles; t += gridDim.x) {
+    cp_async_wait_all();  // this thread's copies of tile t have landed
+    const uint32_t* ring = S.ring[slot];
+    uint32_t u[kExpandItems], wv[kExpandItems];
+#pragma unroll
+    for (int it = 0; it < kExpandItems; ++it) {
+      const int r = it * kExpandBlock + threadIdx.x;
+      u[it] = r < span ? ring[r] : 0u;
+      wv[it] = r < span ? visited[u[it] >> 5] : 0xFFFFFFFFu;
+    }
+    // stage the next tile while the probes are in flight
+    const int64_t tn = t + gridDim.x;
+    const int span_next =
+        tn < ntiles ? stage_tile<kParents>(v, adj, S, slot ^ 1, tn, ntiles, T, qc, tag, pol) : 0;
+#pragma unroll
+    for (int it = 0; it < kExpandItems; ++it) {
       const uint32_t bit = 1u << (u[it] & 31);
       if (!(wv[it] & bit)) {
-        if (kParents) {
-          if (!(atomicOr(&visited[u[it] >> 5], bit) & bit)) parent[u[it]] = src[it];
-        } else {
+        atomicOr(&visited[u[it] >> 5], bit);
+        if (kParents) parent[u[it]] = S.ring_src[slot][it * kExpandBlock + threadIdx.x];
+      }
+    }
+    span = span_next;
+    slot ^= 1;
+  }
+}
+
+template <bool kParents>
+constexpr size_t expand_smem_bytes() { return sizeof(ExpandSmem<kParents>); }
+
+// Warp-centric phase 1: one warp per 2048-edge tile, in 8 rounds of 256
+// edges (8 per lane, lane-interleaved so adjacency loads coalesce).  No
+// shared memory and no block barriers: each round resolves its edges' rows
+// in registers.  Lane j loads row rb+j of the frontier queue (its degree
+// prefix, adjacency base and vertex); the starts of rows rb+1..rb+30 that fall
+// inside the round become bits of eight 32-bit masks (one warp OR-reduction
+// per 32 positions); an edge's row is rb + the number of row starts at or
+// before it (popc), and its base comes from that row's lane by shuffle.  A
+// round spanning more than 31 rows (average degree < 8) takes further
+// batches of 31 rows.  Every reached vertex other than an isolated root has
+// degree >= 1, so row starts are distinct.
+#ifndef BFB_EXPAND_WARP_MINB
+#define BFB_EXPAND_WARP_MINB 4
+#endif
+constexpr int kRound = 256;                      // edges per warp round
+constexpr int kRoundsPerTile = (int)(kTile / kRound);
+
+template <bool kParents>
+__global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_WARP_MINB)
+    k_expand_w(PartView v, const uint32_t* __restrict__ adj) {
+  const int64_t T = v.ctr->q_edges;
+  if (T == 0) return;
+  const int64_t qc = v.ctr->q_count;
+  const int64_t ntiles = (T + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31;
+  const unsigned le_mask = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // bits [0, lane]
+  uint32_t* __restrict__ visited = v.visited;
+  uint32_t* __restrict__ parent = v.parent;
+  const int64_t* __restrict__ q_pre = v.q_pre;
+  const int64_t* __restrict__ q_base = v.q_base;
+  const uint32_t* __restrict__ q_v = v.q_v;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nwarps) {
+    const int64_t e0 = t * kTile;
+    const int64_t span = min((int64_t)kTile, T - e0);
+    const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
+    int64_t cur = v.tile_vstart[t];  // row containing the round's first edge
+    for (int rd = 0; rd < kRoundsPerTile && (int64_t)rd * kRound < span; ++rd) {
+      const int64_t r0 = e0 + (int64_t)rd * kRound;  // global edge index of position 0
+      const int rspan = (int)min((int64_t)kRound, e0 + span - r0);
+      uint32_t u[kExpandItems], src[kExpandItems];
+      unsigned done = 0;  // items whose row is resolved
+      int64_t rb = cur;
+      int lo = 0;  // first position this batch covers
+      while (true) {
+        const int64_t row = rb + lane;
+        const bool valid = row <= ve;
+        const int64_t pre = valid ? __ldg(q_pre + row) : INT64_MAX;
+        const int64_t base = valid ? __ldg(q_base + row) : 0;
+        const uint32_t sv = (kParents && valid) ? __ldg(q_v + row) : 0u;
+        const int64_t relw = pre - r0;
+        const int rel = relw > kRound ? kRound + 1 : (int)relw;  // row start, round-relative
+        const int hi = __shfl_sync(0xffffffffu, rel, 31);       // rows rb..rb+30 end here
+        const int cover_hi = min(hi, kRound);
+        const bool mine = lane >= 1 && lane <= 30 && rel > lo && rel < kRound;
+        unsigned before = 0;
+#pragma unroll
+        for (int it = 0; it < kExpandItems; ++it) {
+          const unsigned bitc = (mine && (rel >> 5) == it) ? (1u << (rel & 31)) : 0u;
+          const unsigned M = __reduce_or_sync(0xffffffffu, bitc);
+          const int r = it * 32 + lane;
+          const int idx = (int)before + __popc(M & le_mask);
+          before += __popc(M);
+          const int64_t b = __shfl_sync(0xffffffffu, base, idx & 31);
+          const uint32_t s = kParents ? __shfl_sync(0xffffffffu, sv, idx & 31) : 0u;
+          if (r >= lo && r < cover_hi && r < rspan) {
+            u[it] = ld_stream_u32(adj + b + r0 + r);
+            src[it] = s;
+            done |= 1u << it;
+          }
+        }
+        if (hi >= rspan) {
+          // next round starts in the row containing position kRound
+          const unsigned last = __ballot_sync(0xffffffffu, rel <= kRound && rel > lo);
+          cur = rb + (31 - __clz((int)(last | 1u)));
+          break;
+        }
+        rb += 31;
+        lo = hi;
+      }
+      uint32_t wv[kExpandItems];
+#pragma unroll
+      for (int it = 0; it < kExpandItems; ++it)
+        wv[it] = ((done >> it) & 1u) ? visited[u[it] >> 5] : 0xFFFFFFFFu;
+#pragma unroll
+      for (int it = 0; it < kExpandItems; ++it) {
+        const uint32_t bit = 1u << (u[it] & 31);
+        if (!(wv[it] & bit)) {
           atomicOr(&visited[u[it] >> 5], bit);
+          if (kParents) parent[u[it]] = src[it];
         }
       }
     }
   }
 }
 
-// Phase 1: one 2048-edge tile per block iteration (load-balanced search over
-// the frontier's degree prefix).  Tiles inside at most kRegSegs frontier rows
-// (hub rows, most of the edges on Kronecker graphs) resolve each edge's row
-// from registers with no shared memory and no block barrier.  Tiles spanning
-// many low-degree rows stage the rows' adjacency bases in shared memory and
-// build an edge -> row owner map (scatter of row starts + block max-scan).
-constexpr int kRegSegs = 4;
-#ifndef BFB_EXPAND_MINB
-#define BFB_EXPAND_MINB 4
+#ifndef BFB_EXPAND_WARP
+#define BFB_EXPAND_WARP 1
 #endif
-constexpr int kExpandMinBlocks = BFB_EXPAND_MINB;  // 4: 64-register cap, 32 warps per SM
+// Launch phase 1 (top-down) for one part on stream s.
+template <bool kParents>
+void launch_expand(int grid, const PartView& v, const uint32_t* adj, cudaStream_t s) {
+  if (BFB_EXPAND_WARP)
+    k_expand_w<kParents><<<grid, kExpandBlock, 0, s>>>(v, adj);
+  else
+    k_expand<kParents><<<grid, kExpandBlock, expand_smem_bytes<kParents>(), s>>>(v, adj);
+}
 
 template <bool kParents>
-__global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartView v,
-                                                         const uint32_t* __restrict__ adj) {
-  __shared__ int32_t s_own[kTile];
-  __shared__ int64_t s_base[kTile + 1];
-  __shared__ uint32_t s_v[kParents ? kTile + 1 : 1];
-  __shared__ int32_t s_wmax[kExpandBlock / 32];
-  const int64_t T = v.ctr->q_edges;
-  if (T == 0) return;
-  const int64_t qc = v.ctr->q_count;
-  const int64_t ntiles = (T + kTile - 1) / kTile;
-  uint32_t* __restrict__ visited = v.visited;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int32_t tag = 0;
-  for (int k = threadIdx.x; k < kTile; k += kExpandBlock) s_own[k] = 0;
-  __syncthreads();
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t e0 = t * kTile;
-    const int span = (int)min((int64_t)kTile, T - e0);
-    const int64_t vs = v.tile_vstart[t];
-    const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
-    const int nseg = (int)(ve - vs + 1);
-    uint32_t u[kExpandItems], src[kExpandItems];
-    unsigned ok = 0;
-    if (nseg <= kRegSegs) {
-      int32_t rel[kRegSegs];
-      int64_t base[kRegSegs];
-      uint32_t sv[kRegSegs];
-#pragma unroll
-      for (int k = 0; k < kRegSegs; ++k) {
-        rel[k] = INT32_MAX;
-        base[k] = 0;
-        sv[k] = 0;
-        if (k < nseg) {
-          const int64_t pre = __ldg(v.q_pre + vs + k);
-          rel[k] = (int32_t)max(pre - e0, (int64_t)INT32_MIN);
-          base[k] = __ldg(v.q_base + vs + k);
-          if (kParents) sv[k] = __ldg(v.q_v + vs + k);
-        }
-      }
-#pragma unroll
-      for (int it = 0; it < kExpandItems; ++it) {
-        const int r = it * kExpandBlock + threadIdx.x;
-        if (r < span) {
-          int64_t b = base[0];
-          uint32_t s0 = sv[0];
-#pragma unroll
-          for (int k = 1; k < kRegSegs; ++k)
-            if (r >= rel[k]) {
-              b = base[k];
-              s0 = sv[k];
-            }
-          u[it] = ld_stream_u32(adj + b + e0 + r);
-          src[it] = s0;
-          ok |= 1u << it;
-        }
-      }
-      claim_batch<kParents>(u, src, ok, visited, v.parent);
-      continue;
-    }
-    // Owner map: row starts scattered with a per-tile tag in the high bits,
-    // so the block max-scan ignores entries left by earlier tiles (no reset).
-    ++tag;
-    const int32_t tg = tag << 12;
-    if (threadIdx.x == 0) s_own[0] = tg;
-    for (int k = threadIdx.x; k < nseg; k += kExpandBlock) {
-      const int64_t pre = v.q_pre[vs + k];
-      s_base[k] = v.q_base[vs + k];
-      if (kParents) s_v[k] = v.q_v[vs + k];
-      const int64_t r = pre - e0;
-      if (r > 0 && r < span) s_own[r] = tg | k;
-    }
-    __syncthreads();
-    {  // inclusive max-scan of the owner map, kTile / kExpandBlock entries per thread
-      constexpr int kPer = kTile / kExpandBlock;
-      int32_t loc[kPer];
-      int32_t run = 0;
-#pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        run = max(run, s_own[threadIdx.x * kPer + i]);
-        loc[i] = run;
-      }
-      int32_t inc = run;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc = max(inc, o);
-      }
-      if (lane == 31) s_wmax[warp] = inc;
-      __syncthreads();
-      int32_t carry = 0;
-      for (int w = 0; w < warp; ++w) carry = max(carry, s_wmax[w]);
-      const int32_t up = __shfl_up_sync(0xffffffffu, inc, 1);
-      const int32_t prev = max(carry, lane > 0 ? up : 0);
-#pragma unroll
-      for (int i = 0; i < kPer; ++i) s_own[threadIdx.x * kPer + i] = max(prev, loc[i]) & 0xFFF;
-      __syncthreads();
-    }
-#pragma unroll
-    for (int it = 0; it < kExpandItems; ++it) {
-      const int r = it * kExpandBlock + threadIdx.x;
-      if (r < span) {
-        const int sg = s_own[r];
-        u[it] = ld_stream_u32(adj + s_base[sg] + e0 + r);
-        src[it] = kParents ? s_v[sg] : 0u;
-        ok |= 1u << it;
-      }
-    }
-    claim_batch<kParents>(u, src, ok, visited, v.parent);
-    __syncthreads();
-  }
+int expand_occupancy(int* occ) {
+  BFB_CUDA(cudaFuncSetAttribute(k_expand<kParents>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)expand_smem_bytes<kParents>()));
+  if (BFB_EXPAND_WARP)
+    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents>,
+                                                           kExpandBlock, 0));
+  else
+    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand<kParents>, kExpandBlock,
+                                                           expand_smem_bytes<kParents>()));
+  return BFB_OK;
 }
 
 // ------------------------------------------------------------ phase 2 ----
@@ -971,9 +1143,9 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
   BFB_CUDA(cudaMallocHost(&ctx->pinned, sizeof(int64_t) * (8 + 8 * (size_t)parts)));
   int occ = 0;
   if (want_parents)
-    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<true>, kExpandBlock, 0));
+    BFB_TRY(expand_occupancy<true>(&occ));
   else
-    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<false>, kExpandBlock, 0));
+    BFB_TRY(expand_occupancy<false>(&occ));
   // Developer knobs for tuning runs: cap resident expand blocks per SM and
   // the shared-memory carveout (percent); unset = occupancy maximum.
   if (const char* e = std::getenv("BFB_EXPAND_OCC")) occ = std::min(occ, std::max(1, std::atoi(e)));
@@ -1050,9 +1222,9 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
         else
           k_bottom_up<false><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
       } else if (ctx->want_parents) {
-        k_expand<true><<<ctx->expand_grid, kExpandBlock, 0, s>>>(v, ctx->g.adj.p);
+        launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, s);
       } else {
-        k_expand<false><<<ctx->expand_grid, kExpandBlock, 0, s>>>(v, ctx->g.adj.p);
+        launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, s);
       }
       ++launches;
       ++expand_launches;
@@ -1360,9 +1532,9 @@ int rank_begin(bfb_ctx* ctx, int64_t root) {
 int rank_expand(bfb_ctx* ctx) {
   PartView v = view_of(ctx, ctx->parts[0]);
   if (ctx->want_parents)
-    k_expand<true><<<ctx->expand_grid, kExpandBlock, 0, ctx->stream>>>(v, ctx->g.adj.p);
+    launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, ctx->stream);
   else
-    k_expand<false><<<ctx->expand_grid, kExpandBlock, 0, ctx->stream>>>(v, ctx->g.adj.p);
+    launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, ctx->stream);
   ++ctx->tables->launches;
   BFB_CUDA(cudaGetLastError());
   return BFB_OK;
