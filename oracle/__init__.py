@@ -7,6 +7,9 @@ that the CUDA library implements:
   (RMAT generator, symmetrize, build_csr, partition_1d), restated.
 * ``oracle.bfs``      -- the bfs-oracle module (``SPEC.md:122-176``,
   Alg. 1 ``PAPER.md:100-138``): ``bfs_top_down`` / ``frontier_sizes``.
+* ``oracle.cbfs``     -- the same top-down BFS restated in C + OpenMP
+  (``bfs_omp.c``, all host threads: the paper's OpenMP worker model,
+  ``PAPER.md:585``); bench.py's timed CPU baseline and reference arm.
 * ``oracle.schedule`` -- the butterfly-schedule module (``SPEC.md:178-265``).
 * ``oracle.engine``   -- the lockstep multi-node engine (``SPEC.md:267-367``,
   Alg. 2 ``PAPER.md:279-374``) with ``RunStats`` accounting.

@@ -57,6 +57,7 @@ struct PartView {
   int64_t *udeg, *upos, *uepre, *tcnt, *tdeg;
   PartCounters* ctr;
   const int64_t* off;  // CSR offsets (rows of q_v)
+  bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
 PartView view_of(bfb_ctx* ctx, Part& p) {
@@ -87,6 +88,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.tdeg = v.tcnt + nt;
   v.ctr = p.ctr.p;
   v.off = ctx->g.offsets.p;
+  v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
 
@@ -336,6 +338,9 @@ constexpr size_t expand_smem_bytes() { return sizeof(ExpandSmem<kParents>); }
 // round spanning more than 31 rows (average degree < 8) takes further
 // batches of 31 rows.  Every reached vertex other than an isolated root has
 // degree >= 1, so row starts are distinct.
+#ifndef BFB_EXPAND_DEFER
+#define BFB_EXPAND_DEFER 0  // 1: resolve all rows of a round first, then issue its loads
+#endif
 #ifndef BFB_EXPAND_WARP_MINB
 #define BFB_EXPAND_WARP_MINB 4
 #endif
@@ -347,53 +352,59 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_WARP_MINB)
     k_expand_w(PartView v, const uint32_t* __restrict__ adj) {
   const int64_t T = v.ctr->q_edges;
   if (T == 0) return;
-  const int64_t qc = v.ctr->q_count;
+  const uint32_t qlast = (uint32_t)(v.ctr->q_count - 1);
   const int64_t ntiles = (T + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31;
   const unsigned le_mask = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // bits [0, lane]
   uint32_t* __restrict__ visited = v.visited;
-  uint32_t* __restrict__ parent = v.parent;
-  const int64_t* __restrict__ q_pre = v.q_pre;
-  const int64_t* __restrict__ q_base = v.q_base;
-  const uint32_t* __restrict__ q_v = v.q_v;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nwarps) {
     const int64_t e0 = t * kTile;
-    const int64_t span = min((int64_t)kTile, T - e0);
-    const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
-    int64_t cur = v.tile_vstart[t];  // row containing the round's first edge
-    for (int rd = 0; rd < kRoundsPerTile && (int64_t)rd * kRound < span; ++rd) {
-      const int64_t r0 = e0 + (int64_t)rd * kRound;  // global edge index of position 0
-      const int rspan = (int)min((int64_t)kRound, e0 + span - r0);
-      uint32_t u[kExpandItems], src[kExpandItems];
-      unsigned done = 0;  // items whose row is resolved
-      int64_t rb = cur;
+    const int span = (int)min((int64_t)kTile, T - e0);
+    const uint32_t vs = v.tile_vstart[t];
+    const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
+    uint32_t cur = vs;  // row containing the round's first edge
+    for (int rd = 0; rd * kRound < span; ++rd) {
+      const int64_t r0 = e0 + rd * kRound;  // global edge index of position 0
+      const int rspan = min(kRound, span - rd * kRound);
+      uint32_t u[kExpandItems];
+#if BFB_EXPAND_DEFER
+      int64_t addr[kExpandItems];
+#endif
+      uint32_t rows[kExpandItems / 2];  // parents: row - vs, 16 bits per item
+      unsigned done = 0;                // items whose row is resolved
+      uint32_t rb = cur;
       int lo = 0;  // first position this batch covers
       while (true) {
-        const int64_t row = rb + lane;
+        const uint32_t row = rb + lane;
         const bool valid = row <= ve;
-        const int64_t pre = valid ? __ldg(q_pre + row) : INT64_MAX;
-        const int64_t base = valid ? __ldg(q_base + row) : 0;
-        const uint32_t sv = (kParents && valid) ? __ldg(q_v + row) : 0u;
+        const int64_t pre = valid ? __ldg(v.q_pre + row) : INT64_MAX;
+        const int64_t base = valid ? __ldg(v.q_base + row) : 0;
         const int64_t relw = pre - r0;
         const int rel = relw > kRound ? kRound + 1 : (int)relw;  // row start, round-relative
         const int hi = __shfl_sync(0xffffffffu, rel, 31);       // rows rb..rb+30 end here
-        const int cover_hi = min(hi, kRound);
+        const int cover_hi = min(min(hi, kRound), rspan);
         const bool mine = lane >= 1 && lane <= 30 && rel > lo && rel < kRound;
         unsigned before = 0;
 #pragma unroll
         for (int it = 0; it < kExpandItems; ++it) {
-          const unsigned bitc = (mine && (rel >> 5) == it) ? (1u << (rel & 31)) : 0u;
-          const unsigned M = __reduce_or_sync(0xffffffffu, bitc);
+          const unsigned M = __reduce_or_sync(0xffffffffu, (mine && (rel >> 5) == it) ? (1u << (rel & 31)) : 0u);
           const int r = it * 32 + lane;
           const int idx = (int)before + __popc(M & le_mask);
           before += __popc(M);
-          const int64_t b = __shfl_sync(0xffffffffu, base, idx & 31);
-          const uint32_t s = kParents ? __shfl_sync(0xffffffffu, sv, idx & 31) : 0u;
-          if (r >= lo && r < cover_hi && r < rspan) {
+          const int64_t b = __shfl_sync(0xffffffffu, base, idx);
+          if (r >= lo && r < cover_hi) {
+#if BFB_EXPAND_DEFER
+            addr[it] = b + r0 + r;
+#else
             u[it] = ld_stream_u32(adj + b + r0 + r);
-            src[it] = s;
+#endif
             done |= 1u << it;
+            if (kParents) {
+              const uint32_t ro = rb + idx - vs;
+              rows[it >> 1] = (it & 1) ? ((rows[it >> 1] & 0xFFFFu) | (ro << 16))
+                                       : ((rows[it >> 1] & 0xFFFF0000u) | ro);
+            }
           }
         }
         if (hi >= rspan) {
@@ -406,6 +417,11 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_WARP_MINB)
         lo = hi;
       }
       uint32_t wv[kExpandItems];
+#if BFB_EXPAND_DEFER
+#pragma unroll
+      for (int it = 0; it < kExpandItems; ++it)
+        if ((done >> it) & 1u) u[it] = ld_stream_u32(adj + addr[it]);
+#endif
 #pragma unroll
       for (int it = 0; it < kExpandItems; ++it)
         wv[it] = ((done >> it) & 1u) ? visited[u[it] >> 5] : 0xFFFFFFFFu;
@@ -414,7 +430,10 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_WARP_MINB)
         const uint32_t bit = 1u << (u[it] & 31);
         if (!(wv[it] & bit)) {
           atomicOr(&visited[u[it] >> 5], bit);
-          if (kParents) parent[u[it]] = src[it];
+          if (kParents) {
+            const uint32_t ro = (rows[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
+            v.parent[u[it]] = __ldg(v.q_v + vs + ro);
+          }
         }
       }
     }
@@ -666,76 +685,78 @@ __global__ void __launch_bounds__(256) k_unit_scan_apply(PartView v) {
   }
 }
 
-// Write pass.  Lane = word computes each word's (count, degree) prefix inside
-// the unit; the stores then run lane = bit, kCommitBatch words at a time, so
-// level / q_v / q_pre / q_base stores are coalesced and the batch's offsets
-// loads are all in flight together (the words are independent once their
-// prefixes are known).
-#ifndef BFB_COMMIT_BATCH
-#define BFB_COMMIT_BATCH 4
-#endif
-constexpr int kCommitBatch = BFB_COMMIT_BATCH;
-
+// Write pass, per 32-word unit (1024 vertices) and warp:
+//   1. levels of every new vertex (lane = bit, one coalesced store per word);
+//   2. the owned new vertices compacted into a per-warp shared list in
+//      ascending order (lane = word: position = prefix of the words' counts);
+//   3. the list, 32 vertices at a time, lane = vertex: offsets pair, a warp
+//      scan of the degrees continuing the unit's edge prefix, and coalesced
+//      q_v / q_pre / q_base stores; tile starts for the tiles whose first edge
+//      falls in the vertex's row.
+// A 32-vertex degree sum fits 32 bits when max degree < 2^26 (kWide = false).
+template <bool kWide>
 __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
                                                       uint32_t next_level) {
+  __shared__ uint32_t s_list[256 / 32][1024];
   const int lane = threadIdx.x & 31;
+  uint32_t* list = s_list[threadIdx.x >> 5];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t unit = gw; unit < v.nunits; unit += nw) {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
-    const unsigned m = __ballot_sync(0xffffffffu, nb != 0);
+    unsigned m = __ballot_sync(0xffffffffu, nb != 0);
     if (!m) continue;
     const int64_t w0 = v.abase + unit * 32;
-    const int64_t dsum = own ? word_degree_sum(own, (w0 + lane) << 5, off) : 0;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
+      if ((x >> lane) & 1u) v.level[((w0 + j) << 5) + lane] = next_level;
+    }
     const int cnt = __popc(own);
-    int cinc = cnt;
+    int pos = cnt;
 #pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, cinc, dd);
-      if (lane >= dd) cinc += t;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, pos, d);
+      if (lane >= d) pos += t;
     }
-    const int64_t dinc_w = warp_inclusive_i64(dsum);
-    const int64_t wpos = v.upos[unit] + (cinc - cnt);      // this lane's word: first position
-    const int64_t wepre = v.uepre[unit] + (dinc_w - dsum);  // ... and first edge prefix
-#pragma unroll 1
-    for (int g = 0; g < 32; g += kCommitBatch) {
-      if (!((m >> g) & ((1u << kCommitBatch) - 1u))) continue;
-      uint32_t x[kCommitBatch], xo[kCommitBatch];
-      int64_t r0[kCommitBatch], d[kCommitBatch];
+    const int total = __shfl_sync(0xffffffffu, pos, 31);
+    pos -= cnt;
+    for (uint32_t x = own; x; x &= x - 1) list[pos++] = (uint32_t)(((w0 + lane) << 5) + __ffs(x) - 1);
+    __syncwarp();
+    const int64_t p0 = v.upos[unit];
+    int64_t ecarry = v.uepre[unit];
+    for (int i = 0; i < total; i += 32) {
+      const int k = i + lane;
+      const bool ok = k < total;
+      const uint32_t u = ok ? list[k] : 0u;
+      const int64_t o0 = ok ? __ldg(off + u) : 0;
+      const int64_t d = ok ? __ldg(off + u + 1) - o0 : 0;
+      int64_t inc;
+      if (kWide) {
+        inc = warp_inclusive_i64(d);
+      } else {
+        int x = (int)d;
 #pragma unroll
-      for (int k = 0; k < kCommitBatch; ++k) {
-        x[k] = __shfl_sync(0xffffffffu, nb, g + k);
-        xo[k] = __shfl_sync(0xffffffffu, own, g + k);
-        const int64_t u = ((w0 + g + k) << 5) + lane;
-        r0[k] = 0;
-        d[k] = 0;
-        if ((xo[k] >> lane) & 1u) {
-          r0[k] = __ldg(off + u);
-          d[k] = __ldg(off + u + 1) - r0[k];
+        for (int s2 = 1; s2 < 32; s2 <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, x, s2);
+          if (lane >= s2) x += t;
         }
+        inc = x;
       }
-#pragma unroll
-      for (int k = 0; k < kCommitBatch; ++k) {
-        const int64_t u = ((w0 + g + k) << 5) + lane;
-        if ((x[k] >> lane) & 1u) v.level[u] = next_level;
-        const int64_t p0 = __shfl_sync(0xffffffffu, wpos, g + k);
-        const int64_t e0 = __shfl_sync(0xffffffffu, wepre, g + k);
-        if (xo[k]) {
-          const int64_t dinc = warp_inclusive_i64(d[k]);
-          if ((xo[k] >> lane) & 1u) {
-            const int64_t p = p0 + __popc(xo[k] & lt);
-            const int64_t e = e0 + dinc - d[k];
-            v.q_v[p] = (uint32_t)u;
-            v.q_pre[p] = e;
-            v.q_base[p] = r0[k] - e;
-            for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d[k]; ++t)
-              v.tile_vstart[t] = (uint32_t)p;
-          }
-        }
+      if (ok) {
+        const int64_t e = ecarry + inc - d;
+        const int64_t p = p0 + k;
+        v.q_v[p] = u;
+        v.q_pre[p] = e;
+        v.q_base[p] = o0 - e;
+        for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d; ++t) v.tile_vstart[t] = (uint32_t)p;
       }
+      ecarry += __shfl_sync(0xffffffffu, inc, 31);
     }
+    __syncwarp();
     if (nb) {
       v.start[w0 + lane] = a;
       if (v.front) v.front[w0 + lane] = nb;
@@ -959,7 +980,10 @@ int launch_commit_write(const PartView& v, const int64_t* off, uint32_t next_lev
     return 1;
   }
   k_unit_scan_apply<<<(unsigned)ntiles, 256, 0, s>>>(v);
-  k_commit_write<<<grid, 256, 0, s>>>(v, off, next_level);
+  if (v.wide)
+    k_commit_write<true><<<grid, 256, 0, s>>>(v, off, next_level);
+  else
+    k_commit_write<false><<<grid, 256, 0, s>>>(v, off, next_level);
   return 2;
 }
 

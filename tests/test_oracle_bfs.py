@@ -55,6 +55,29 @@ def test_golden_levels(golden):
             assert ob.traversed_edges(off, d) == want["traversed_edges"]
 
 
+def test_c_oracle_golden_levels(golden):
+    # the C/OpenMP restatement (bench.py's CPU baseline) against the same
+    # golden levels, on 1 thread and on all host threads
+    from oracle import cbfs
+
+    for key in ("s12_ef8", "s16_ef8"):
+        e = golden[key]
+        off, adj = util.rmat_graph(e["scale"], e["edge_factor"], e["seed"])
+        for r, want in e["bfs"].items():
+            for threads in (1, 0):
+                d = cbfs.bfs_top_down(off, adj, int(r), threads=threads)
+                assert util.sha16(d) == want["levels_sha"], (key, r, threads)
+    off, adj = util.path_graph(3)
+    assert cbfs.bfs_top_down(off, adj, 0).tolist() == [0, 1, 2]
+    off, adj = util.csr_of_undirected(4, [(0, 1), (2, 3)])
+    assert cbfs.bfs_top_down(off, adj, 0).tolist() == [0, 1, U, U]
+    with pytest.raises(ValueError):
+        cbfs.bfs_top_down(off, adj, 4)
+    off, adj = util.rmat_graph(14)
+    d, scanned, secs, done = cbfs.bfs_top_down(off, adj, 0, time_budget_s=60)
+    assert done and scanned == ob.traversed_edges(off, d)
+
+
 def test_time_budget_sample():
     off, adj = util.rmat_graph(14)
     d, scanned, secs, done = ob.bfs_top_down(off, adj, 0, time_budget_s=60)

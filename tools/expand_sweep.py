@@ -27,10 +27,11 @@ for parents, direction in ((False, "top-down"), (True, "top-down"), (True, "opti
 ''' % ROOT
 
 if __name__ == "__main__":
-    settings = []
-    for lib in sys.argv[1:] or ["libbflybfs.so"]:
-        for persist in ("0",):
-            settings.append((lib, persist))
-    for lib, persist in settings:
-        env = dict(os.environ, BFB_LIB=lib, BFB_L2_PERSIST=persist, SW_TAG=f"{lib} persist={persist}")
+    # each argument: LIB[:VAR=VALUE[,VAR=VALUE...]]
+    for spec in sys.argv[1:] or ["libbflybfs.so"]:
+        lib, _, extra = spec.partition(":")
+        env = dict(os.environ, BFB_LIB=lib, SW_TAG=spec)
+        for kv in filter(None, extra.split(",")):
+            k, _, val = kv.partition("=")
+            env[k] = val
         subprocess.run([sys.executable, "-c", BODY], env=env, timeout=600)
