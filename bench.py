@@ -229,6 +229,9 @@ def main():
         bracket_ms = dg.timer_stop()
     value = hmean(teps)
     peak, peak_src = measured_peaks()
+    # the expand's real ceiling: one random visited-bitmap probe per edge
+    probe_peak = dg.probe_peak((g.num_vertices + 7) // 8)
+    probe_achieved = sum(edges) / (exp_ms * 1e-3)
     achieved = level_bytes / (exp_ms * 1e-3) / 1e9 if exp_ms > 0 else 0.0
     traffic = committed_traffic(args.scale, args.edge_factor)
 
@@ -292,7 +295,14 @@ def main():
                                      "sum of k_expand event time",
                      "peak_src": peak_src,
                      "expand_share": round(exp_ms / sum(times), 4),
-                     "expand_launches_per_bfs": exp_launch / K},
+                     "expand_launches_per_bfs": exp_launch / K,
+                     "l2_probe": {"achieved": round(probe_achieved / 1e9, 2),
+                                  "peak": round(probe_peak / 1e9, 2), "unit": "Gprobe/s",
+                                  "frac": round(probe_achieved / probe_peak, 4),
+                                  "def": "one random 4 B visited-bitmap load per traversed "
+                                         "edge / k_expand time, vs random 4 B loads over a "
+                                         "bitmap-sized (n/8 B) buffer, measured in this run "
+                                         "(csrc/probe_peak.cu)"}},
         "cpu_baseline": {"value": round(cpu_v, 5), "unit": UNIT, "cores": cpu_threads(),
                          "kind": "port",
                          "sample": f"oracle/bfs_omp.c top-down BFS (C + OpenMP, {cpu_threads()} "

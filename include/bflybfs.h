@@ -160,6 +160,11 @@ int bfb_copy_parents(bfb_ctx* ctx, int64_t* parents_out);
  * 4 edge spans >1 level, 8 reached vertex without predecessor, 16 bad parent). */
 int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out);
 
+/* Measurement helper (bench.py roofline, not part of the reference API): the
+ * random-probe ceiling of phase 1 -- random 4-byte loads over a `bytes`-sized
+ * device buffer (the visited bitmap's size).  *probes_out loads took *ms_out. */
+int bfb_probe_peak(bfb_ctx* ctx, int64_t bytes, int64_t* probes_out, double* ms_out);
+
 /* ---- multi-process mode: one process per GPU (torchrun), node = rank -----
  * The host driver (paper_2103_13577_b200/dist.py) sequences one level as
  * expand -> for each butterfly round: publish, [barrier + snapshot-size

@@ -88,6 +88,7 @@ _SIGNATURES = {
     "bfb_copy_levels": (c_int, [c_void_p, _U32P]),
     "bfb_copy_parents": (c_int, [c_void_p, _I64P]),
     "bfb_validate": (c_int, [c_void_p, c_int64, _I64P]),
+    "bfb_probe_peak": (c_int, [c_void_p, c_int64, _I64P, POINTER(c_double)]),
     "bfb_rank_setup": (c_int, [c_void_p, c_int, _I64P, c_int, c_int, c_int, c_int]),
     "bfb_rank_ipc_handles": (c_int, [c_void_p, c_void_p]),
     "bfb_rank_open_peer": (c_int, [c_void_p, c_int, c_void_p]),

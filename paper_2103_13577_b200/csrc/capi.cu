@@ -344,6 +344,12 @@ int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out) {
   return engine_validate(ctx, root, errors_out);
 }
 
+int bfb_probe_peak(bfb_ctx* ctx, int64_t bytes, int64_t* probes_out, double* ms_out) {
+  CTX_GUARD(ctx);
+  if (!probes_out || !ms_out || bytes <= 0) return fail(BFB_ERR_INVALID, "bad arguments");
+  return probe_peak(ctx, bytes, probes_out, ms_out);
+}
+
 int bfb_rank_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int fanout,
                    int strategy, int want_parents, int rank) {
   CTX_GUARD(ctx);

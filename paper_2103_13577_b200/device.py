@@ -27,13 +27,16 @@ class _PinnedPool:
     def array(self, count, dtype):
         dtype = np.dtype(dtype)
         nbytes = int(count) * dtype.itemsize
-        lst = self._free.get(nbytes)
-        if lst:
-            addr = lst.pop()
-        else:
-            p = c_void_p()
-            check(_lib.load().bfb_host_alloc(max(nbytes, 1), byref(p)))
-            addr = p.value
+        lst = self._free.setdefault(nbytes, [])
+        if not lst:
+            # first request of this size: allocate a spare too, so a caller
+            # that still holds the previous result never waits on
+            # cudaHostAlloc (hundreds of ms for GB-sized buffers)
+            for _ in range(2):
+                p = c_void_p()
+                check(_lib.load().bfb_host_alloc(max(nbytes, 1), byref(p)))
+                lst.append(p.value)
+        addr = lst.pop()
         buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(addr)
         weakref.finalize(buf, self._release, nbytes, addr)
         return np.frombuffer(buf, dtype=dtype, count=int(count))
@@ -204,6 +207,13 @@ class DeviceGraph:
         ms = ctypes.c_double()
         check(_lib.load().bfb_timer_stop(self.handle, byref(ms)))
         return ms.value
+
+    def probe_peak(self, nbytes):
+        """Random 4-byte loads per second over an nbytes device buffer (the
+        phase-1 probe ceiling; see csrc/probe_peak.cu)."""
+        n, ms = c_int64(), ctypes.c_double()
+        check(_lib.load().bfb_probe_peak(self.handle, int(nbytes), byref(n), byref(ms)))
+        return n.value / (ms.value * 1e-3)
 
     def set_timing(self, enabled):
         check(_lib.load().bfb_set_timing(self.handle, 1 if enabled else 0))
