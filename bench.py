@@ -191,9 +191,7 @@ def main():
         return
 
     if ws > 1:
-        from paper_2103_13577_b200 import dist
-
-        line = dist.bench_rank(args, cfg, METRIC, UNIT)
+        line = main_rank(args, cfg)
         if rank == 0 and line is not None:
             print(json.dumps(line), flush=True)
         return
@@ -319,6 +317,123 @@ def main():
         "direction_optimizing": direction_opt,
     }
     print(json.dumps(line), flush=True)
+
+
+def main_rank(args, cfg):
+    """N > 1 under torchrun: one rank per GPU, node = rank.  The s29 graph is
+    built on every GPU (deterministic); each rank keeps its partition_1d rows.
+    A step = one BFS through the device-synchronised engine (bfb_rank_bfs:
+    per-round barrier and snapshot sizes through NVLink mailboxes, snapshots
+    merged in place from peer HBM); t = max over ranks of the device time from
+    root injection to termination.  Returns rank 0's JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_13577_b200 import dist as bdist
+    from paper_2103_13577_b200 import graphs
+
+    ws, rank, local = dist_env()
+    dev = int(os.environ.get("BFB_DEVICE", str(local)))
+    torch.cuda.set_device(dev)
+    if not dist.is_initialized():
+        backend = os.environ.get("BFB_DIST_BACKEND", "nccl")  # gloo: several ranks per GPU
+        if backend == "nccl":
+            dist.init_process_group(backend="nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend=backend)
+    comm = bdist.Comm()
+    P = comm.size
+    fanout = args.fanout or min(2, P)
+    parents = not args.no_parents
+    t0 = time.time()
+    g = graphs.kronecker(args.scale, args.edge_factor, 1, device=dev)
+    dg = g.device
+    build_s = time.time() - t0
+    b = dg.partition_1d(P)
+    roots = graphs.sample_roots(g, args.roots)
+    eng = bdist.RankEngine(dg, b, fanout, "butterfly", parents, comm)
+    dg.set_timing(True)
+    K, W = args.steps, args.warmup
+
+    def timed(direction):
+        dg.set_direction(direction)
+        for i in range(W):
+            eng.node.bfs(int(roots[(K + i) % len(roots)]))
+        comm.barrier()
+        out = {"teps": [], "edges": [], "t": [], "launches": 0, "expand": 0.0, "exchange": 0.0,
+               "commit": 0.0, "bu": 0, "reached": 0}
+        dg.timer_start()
+        for i in range(K):
+            sizes, st = eng.node.bfs(int(roots[i % len(roots)]))
+            tmax = comm.allreduce(float(st.elapsed_ms), "max")
+            e = int(comm.allreduce(int(st.traversed_edges)))
+            out["teps"].append(e / (tmax * 1e-3) / 1e9)
+            out["edges"].append(e)
+            out["t"].append(tmax)
+            out["launches"] += int(st.kernel_launches)
+            out["expand"] += comm.allreduce(float(st.expand_ms), "max")
+            out["exchange"] += comm.allreduce(float(st.exchange_ms), "max")
+            out["commit"] += comm.allreduce(float(st.commit_ms), "max")
+            out["bu"] += int(st.bottom_up_levels)
+            out["reached"] += sum(sizes)
+        out["bracket"] = comm.allreduce(dg.timer_stop(), "max")
+        return out
+
+    with ClockSampler(dev) as clk:
+        td = timed("top-down")
+    do = timed("optimizing")
+    dg.set_direction("top-down")
+    value = hmean(td["teps"])
+    peak, peak_src = measured_peaks()
+    # per-rank algorithmic expand bytes (4 B/edge + 24 B per owned reached
+    # vertex, summed over ranks) over the slowest rank's expand time
+    level_bytes = 4 * sum(td["edges"]) + (24 if parents else 20) * td["reached"]
+    achieved = level_bytes / P / (td["expand"] * 1e-3) / 1e9 if td["expand"] > 0 else 0.0
+
+    # e2e: the public multi-rank API (every rank calls RankEngine.run(root) and
+    # gets the DistanceArray in host numpy); wall clock, max over ranks
+    e2e = []
+    eng.run(int(roots[0]), parents=False)
+    for i in range(min(args.e2e_steps, K)):
+        r = int(roots[i % len(roots)])
+        comm.barrier()
+        t = time.perf_counter()
+        d, st = eng.run(r, parents=False)  # the reference's contract: levels only
+        dt = comm.allreduce(time.perf_counter() - t, "max")
+        e2e.append(st.traversed_edges / dt / 1e9)
+
+    cfg = dict(cfg, fanout=fanout, num_parts=P)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": P, "steps": K,
+        "warmup": W, "ms_per_step": round(td["bracket"] / K, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": cfg,
+        "aggregate_gteps": round(sum(td["edges"]) / (td["bracket"] * 1e-3) / 1e9, 3),
+        "bfs_ms_mean": round(float(np.mean(td["t"])), 4),
+        "phase_ms_mean_max_over_ranks": {k: round(td[k] / K, 4)
+                                         for k in ("expand", "exchange", "commit")},
+        "graph": {"num_vertices": g.num_vertices, "num_edges": g.num_edges,
+                  "build_s": round(build_s, 2), "max_degree": dg.max_degree},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "k_expand_w (phase 1 top-down expansion), per GPU",
+                     "achieved_def": "(4 B x edges + 24 B x reached vertices) / N per GPU / "
+                                     "slowest rank's expand time",
+                     "peak_src": peak_src},
+        "cpu_baseline": None,
+        "e2e": {"value": round(hmean(e2e), 3), "unit": UNIT, "h2d_bytes_per_step": 8 * P,
+                "d2h_bytes_per_step": 4 * g.num_vertices * P, "steps": len(e2e),
+                "path": "paper_2103_13577_b200.dist.RankEngine.run(root) on every rank -> "
+                        "DistanceArray in host numpy, wall clock max over ranks"},
+        "gpu_launches": td["launches"],
+        "clocks": clk.summary(),
+        "exchange": "device-synchronised butterfly: per round publish -> NVLink mailbox signal "
+                    "-> spin-wait -> in-place merge of the sources' snapshot bitmaps (CUDA IPC)",
+        "direction_optimizing": {"value": round(hmean(do["teps"]), 3), "unit": UNIT,
+                                 "bfs_ms_mean": round(float(np.mean(do["t"])), 4),
+                                 "bottom_up_levels_mean_per_rank": round(do["bu"] / K, 2)},
+    }
+    return line if comm.rank == 0 else None
 
 
 def run_reference(args, cfg, n_gpus):

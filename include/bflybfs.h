@@ -175,7 +175,9 @@ int bfb_probe_peak(bfb_ctx* ctx, int64_t bytes, int64_t* probes_out, double* ms_
 /* init's allocation step for node `rank` only (global partition boundaries). */
 int bfb_rank_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int fanout,
                    int strategy, int want_parents, int rank);
-/* 128 bytes: the IPC handles of this node's two (round-parity) snapshot buffers. */
+/* 256 bytes: the IPC handles of this node's two (round-parity) snapshot
+ * buffers, its mailbox (device-synchronised mode) and its parents (zero
+ * without parents). */
 int bfb_rank_ipc_handles(bfb_ctx* ctx, void* handles_out);
 int bfb_rank_open_peer(bfb_ctx* ctx, int peer, const void* handles);
 int bfb_rank_begin(bfb_ctx* ctx, int64_t root);
@@ -192,6 +194,20 @@ int bfb_rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out);
 int bfb_rank_finish(bfb_ctx* ctx, bfb_run_stats* stats_out);
 /* This node's phase-1 parents (uint32, 0xFFFFFFFF = none): min over nodes is
  * a valid parent array. */
+/* One whole BFS for this node with device-side synchronisation: per round,
+ * publish -> signal {seq, snapshot size} into every peer's mailbox (NVLink
+ * stores, release) -> spin on this node's mailbox (acquire) -> merge the
+ * sources' snapshots in place.  No host round trip inside a level; the host
+ * reads the frontier count once per level.  Every rank calls it with the same
+ * root.  sizes_out[0..max_levels) = per_level_frontier_size; stats_out as
+ * bfb_rank_finish plus this node's exchange accounting.  Honours
+ * bfb_set_direction (each node applies Beamer's rule to its own rows). */
+int bfb_rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
+                 bfb_run_stats* stats_out);
+/* Output parents of the last BFS (int64, -1 unreached, root -> root): min over
+ * every node's phase-1 parents, read from the peers' HBM (IPC mappings); call
+ * after all ranks finished the BFS. */
+int bfb_rank_parents(bfb_ctx* ctx, int64_t* parents_out);
 int bfb_rank_parents_raw(bfb_ctx* ctx, uint32_t* parents_out);
 
 #ifdef __cplusplus

@@ -98,6 +98,8 @@ _SIGNATURES = {
     "bfb_rank_merge": (c_int, [c_void_p, c_int, _I32P, _I64P, c_int]),
     "bfb_rank_commit": (c_int, [c_void_p, _I64P, _I64P]),
     "bfb_rank_finish": (c_int, [c_void_p, POINTER(RunStatsC)]),
+    "bfb_rank_bfs": (c_int, [c_void_p, c_int64, _I64P, c_int64, POINTER(RunStatsC)]),
+    "bfb_rank_parents": (c_int, [c_void_p, _I64P]),
     "bfb_rank_parents_raw": (c_int, [c_void_p, _U32P]),
 }
 

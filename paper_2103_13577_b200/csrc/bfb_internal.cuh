@@ -260,6 +260,9 @@ int rank_publish(bfb_ctx* ctx, int parity, int64_t* count_out);
 int rank_merge(bfb_ctx* ctx, int parity, const int32_t* srcs, const int64_t* counts, int nsrc);
 int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out);
 int rank_finish(bfb_ctx* ctx, bfb_run_stats* st);
+int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
+             bfb_run_stats* st);
+int rank_parents(bfb_ctx* ctx, int64_t* out);
 int rank_parents_raw(bfb_ctx* ctx, uint32_t* out);
 
 // schedule (capi.cu)

@@ -1008,6 +1008,15 @@ struct EngineTables {
   int rank = -1;
   std::vector<const uint32_t*> peer_pub[2];  // per node, by round parity
   std::vector<void*> opened;                 // IPC mappings to close
+  // device-synchronised rank mode (rank_bfs): this node's mailbox (one
+  // {seq, count} slot per writer, written by peers over NVLink), the peers'
+  // mailboxes (IPC-mapped), a barrier-timeout flag, and the round counter
+  DevBuf<int64_t> mail;
+  DevBuf<int64_t*> peer_mail_dev;
+  DevBuf<int32_t> err;
+  std::vector<int64_t*> peer_mail;
+  std::vector<uint32_t*> peer_parent;  // every node's phase-1 parents (IPC-mapped)
+  int64_t seq = 0;
   int64_t level = 0, reached = 0, launches = 0, levels = 0;
   int64_t remote_messages = 0, remote_vertices = 0, high_water = 0, exchange_bytes = 0;
   ~EngineTables() {
@@ -1493,14 +1502,31 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   for (int par = 0; par < 2; ++par) D->peer_pub[par].assign(parts, nullptr);
   D->peer_pub[0][rank] = p.pub.p;
   D->peer_pub[1][rank] = p.pub_alt.p;
+  BFB_TRY(D->mail.alloc(4 * (size_t)parts));
+  BFB_CUDA(cudaMemset(D->mail.p, 0, 4 * (size_t)parts * sizeof(int64_t)));
+  BFB_TRY(D->peer_mail_dev.alloc(parts));
+  BFB_TRY(D->err.alloc(1));
+  BFB_CUDA(cudaMemset(D->err.p, 0, sizeof(int32_t)));
+  D->peer_mail.assign(parts, nullptr);
+  D->peer_mail[rank] = D->mail.p;
+  D->peer_parent.assign(parts, nullptr);
+  if (want_parents) {
+    D->peer_parent[rank] = p.parent.p;
+    BFB_TRY(D->parents_final.alloc(n + 1));
+  }
+  D->seq = 0;
+  if (ctx->direction) BFB_CUDA(cudaMemset(p.front.p, 0, nwords_pad * sizeof(uint32_t)));
   return BFB_OK;
 }
 
 int rank_ipc_handles(bfb_ctx* ctx, void* out) {
   if (!ctx->tables || ctx->tables->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
-  cudaIpcMemHandle_t h[2];
+  cudaIpcMemHandle_t h[4];
+  std::memset(h, 0, sizeof(h));
   BFB_CUDA(cudaIpcGetMemHandle(&h[0], ctx->parts[0].pub.p));
   BFB_CUDA(cudaIpcGetMemHandle(&h[1], ctx->parts[0].pub_alt.p));
+  BFB_CUDA(cudaIpcGetMemHandle(&h[2], ctx->tables->mail.p));
+  if (ctx->want_parents) BFB_CUDA(cudaIpcGetMemHandle(&h[3], ctx->parts[0].parent.p));
   std::memcpy(out, h, sizeof(h));
   return BFB_OK;
 }
@@ -1510,13 +1536,18 @@ int rank_open_peer(bfb_ctx* ctx, int peer, const void* handles) {
   if (!D || D->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
   if (peer < 0 || peer >= ctx->num_parts || peer == D->rank)
     return fail(BFB_ERR_INVALID, "bad peer");
-  cudaIpcMemHandle_t h[2];
+  cudaIpcMemHandle_t h[4];
   std::memcpy(h, handles, sizeof(h));
-  for (int par = 0; par < 2; ++par) {
+  for (int k = 0; k < (ctx->want_parents ? 4 : 3); ++k) {
     void* ptr = nullptr;
-    BFB_CUDA(cudaIpcOpenMemHandle(&ptr, h[par], cudaIpcMemLazyEnablePeerAccess));
+    BFB_CUDA(cudaIpcOpenMemHandle(&ptr, h[k], cudaIpcMemLazyEnablePeerAccess));
     D->opened.push_back(ptr);
-    D->peer_pub[par][peer] = static_cast<const uint32_t*>(ptr);
+    if (k < 2)
+      D->peer_pub[k][peer] = static_cast<const uint32_t*>(ptr);
+    else if (k == 2)
+      D->peer_mail[peer] = static_cast<int64_t*>(ptr);
+    else
+      D->peer_parent[peer] = static_cast<uint32_t*>(ptr);
   }
   return BFB_OK;
 }
@@ -1540,6 +1571,7 @@ int rank_begin(bfb_ctx* ctx, int64_t root) {
   BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
   BFB_CUDA(cudaMemsetAsync(p.level.p, 0xFF, n * sizeof(uint32_t), s));
   if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
+  if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
   const int owner = root >= p.lo && root < p.hi;
   k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), ctx->g.offsets.p, root, owner, ctx->run.p);
   BFB_CUDA(cudaGetLastError());
@@ -1664,10 +1696,289 @@ int rank_finish(bfb_ctx* ctx, bfb_run_stats* st) {
   return BFB_OK;
 }
 
+// Output parents of the last rank_bfs: element-wise min over every node's
+// phase-1 parents, read in place from the peers' HBM (all ranks must have
+// finished the BFS -- the caller's barrier).
+int rank_parents(bfb_ctx* ctx, int64_t* out) {
+  EngineTables* D = ctx->tables;
+  if (!D || D->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
+  if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
+  const int P = ctx->num_parts;
+  for (int g = 0; g < P; ++g)
+    if (!D->peer_parent[g]) return fail(BFB_ERR_STATE, "peer parents not mapped");
+  if (D->parents.n < (size_t)P) BFB_TRY(D->parents.alloc(P));
+  BFB_CUDA(cudaMemcpy(D->parents.p, D->peer_parent.data(), P * sizeof(uint32_t*),
+                      cudaMemcpyHostToDevice));
+  const int64_t n = ctx->g.n;
+  k_parents_min<<<grid_cap(n, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
+      D->parents.p, P, n, D->parents_final.p);
+  std::vector<uint32_t> tmp(n);
+  BFB_CUDA(cudaMemcpyAsync(tmp.data(), D->parents_final.p, n * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  BFB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t i = 0; i < n; ++i) out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
+  return BFB_OK;
+}
+
 int rank_parents_raw(bfb_ctx* ctx, uint32_t* out) {
   if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
   BFB_CUDA(cudaMemcpy(out, ctx->parts[0].parent.p, ctx->g.n * sizeof(uint32_t),
                       cudaMemcpyDeviceToHost));
+  return BFB_OK;
+}
+
+
+// ------------------------------------------- device-synchronised rank mode --
+// rank_bfs runs a whole BFS for node `rank` with no host round trip inside a
+// level: each butterfly round is publish -> signal -> wait -> merge, where
+// signal writes {seq, snapshot size} into every peer's mailbox over NVLink
+// (release at system scope) and wait spins (acquire) until every peer's slot
+// in this node's mailbox reached seq -- the Synchronize() of PAPER.md:350 as a
+// device barrier.  The merge then reads the scheduled sources' snapshot
+// bitmaps in place and their sizes from the mailbox (empty sources skipped,
+// SPEC.md:346).  The host syncs once per level, for the frontier count
+// (termination): every node holds the same synchronized
+// frontier after phase 2, so every rank reaches the same decision alone.
+namespace {
+
+__device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+
+// Mailbox slot of writer w: [kMail*w + parity] = snapshot size of w's last
+// round of that parity, [kMail*w + 2] = w's last published round (seq).  The
+// sizes are double-buffered like the snapshots: a writer can run one round
+// ahead of a reader that is still merging, never two.
+constexpr int kMail = 4;
+
+// One thread per peer: write this node's size and seq into its mailbox.
+__global__ void k_signal(int64_t* const* peer_mail, int me, int num_nodes, int64_t seq,
+                         const PartCounters* ctr, int parity) {
+  const int g = threadIdx.x;
+  if (g >= num_nodes || g == me) return;
+  int64_t* slot = peer_mail[g] + kMail * me;
+  slot[parity] = ((volatile const PartCounters*)ctr)->pub_count[parity];
+  st_release_sys(slot + 2, seq);  // orders the snapshot and the size before seq
+}
+
+// Spin until every peer's seq in this node's mailbox reached `seq`; gives up
+// after `timeout_ns` (sets *err) so a lost peer can never hang the GPU.
+__global__ void k_wait(const int64_t* mail, int me, int num_nodes, int64_t seq, int32_t* err,
+                       uint64_t timeout_ns) {
+  const int g = threadIdx.x;
+  if (g >= num_nodes || g == me) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_sys(mail + kMail * g + 2) < seq) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicExch(err, 1);
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
+struct RoundSrc {
+  const uint32_t* pub[kMaxSrc];
+  int id[kMaxSrc];
+  int n;
+};
+
+// OR the non-empty sources' snapshots into visited (this node is the only
+// writer of its bitmap during the merge).
+__global__ void k_merge_mail(RoundSrc R, const int64_t* mail, int parity,
+                             uint32_t* __restrict__ vis, int64_t nwords) {
+  uint64_t live = 0;
+  for (int i = 0; i < R.n; ++i)
+    if (mail[kMail * R.id[i] + parity] > 0) live |= 1ull << i;
+  if (!live) return;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    for (uint64_t m = live; m; m &= m - 1) acc |= R.pub[__ffsll((long long)m) - 1][w];
+    if (acc) {
+      const uint32_t cur = vis[w];
+      if (acc & ~cur) vis[w] = cur | acc;
+    }
+  }
+}
+
+// RunStats accounting of one round from the mailbox sizes (one thread).
+__global__ void k_account_mail(RoundSrc R, const int64_t* mail, int parity, RunCounters* run,
+                               int64_t* hw, int64_t bytes_per_transfer) {
+  if (threadIdx.x) return;
+  int64_t msgs = 0, in = 0;
+  for (int i = 0; i < R.n; ++i) {
+    const int64_t k = mail[kMail * R.id[i] + parity];
+    if (k > 0) {
+      ++msgs;
+      in += k;
+    }
+  }
+  run->remote_messages += msgs;
+  run->remote_vertices += in;
+  run->exchange_bytes += msgs * bytes_per_transfer;
+  if (in > *hw) *hw = in;
+}
+
+}  // namespace
+
+int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
+             bfb_run_stats* st) {
+  EngineTables* D = ctx->tables;
+  if (!D || D->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
+  const int P = ctx->num_parts, me = D->rank;
+  for (int g = 0; g < P; ++g)
+    if (!D->peer_mail[g]) return fail(BFB_ERR_STATE, "peer mailboxes not mapped");
+  BFB_CUDA(cudaMemcpy(D->peer_mail_dev.p, D->peer_mail.data(), P * sizeof(int64_t*),
+                      cudaMemcpyHostToDevice));
+  BFB_TRY(rank_begin(ctx, root));
+  cudaStream_t s = ctx->stream;
+  Part& p = ctx->parts[0];
+  const int64_t n = ctx->g.n, nwords = (n + 31) / 32;
+  const int64_t* off = ctx->g.offsets.p;
+  const int sms = ctx->num_sms;
+  const int64_t bytes_per_transfer = nwords * (int64_t)sizeof(uint32_t);
+  const uint64_t timeout_ns = 60ull * 1000 * 1000 * 1000;
+  BFB_CUDA(cudaMemsetAsync(ctx->high_water.p, 0, sizeof(int64_t), s));
+  std::vector<RoundSrc> rounds;
+  for (auto& rnd : ctx->schedule) {
+    RoundSrc R{};
+    for (int src : rnd[me]) {
+      R.pub[R.n] = nullptr;  // filled per parity below
+      R.id[R.n++] = src;
+    }
+    rounds.push_back(R);
+  }
+  bool bottom_up = ctx->direction == 2;
+  int64_t bu_levels = 0, prev_frontier = 1, nsizes = 1, launches = 0;
+  if (sizes_out && max_levels > 0) sizes_out[0] = 1;
+  const unsigned rest_grid = grid_cap(nwords, 256, sms, 4);
+  double t_expand = 0, t_exchange = 0, t_commit = 0;
+  int64_t expand_launches = 0;
+  while (true) {
+    PartView v = view_of(ctx, p);
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
+    if (bottom_up) {
+      const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo) * 32, 256, sms, 8);
+      unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
+      if (ctx->want_parents)
+        k_bottom_up<true><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+      else
+        k_bottom_up<false><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+      ++bu_levels;
+    } else if (ctx->want_parents) {
+      launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, s);
+    } else {
+      launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, s);
+    }
+    ++launches;
+    ++expand_launches;
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[3], s));
+    for (RoundSrc R : rounds) {
+      const int64_t seq = ++D->seq;
+      const int parity = (int)(seq & 1);
+      PartView pv = v;
+      pv.pub = parity ? p.pub_alt.p : p.pub.p;
+      for (int i = 0; i < R.n; ++i) R.pub[i] = D->peer_pub[parity][R.id[i]];
+      BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_count[parity], 0, sizeof(int64_t), s));
+      k_publish<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(pv, parity);
+      k_signal<<<1, 64, 0, s>>>(D->peer_mail_dev.p, me, P, seq, p.ctr.p, parity);
+      k_wait<<<1, 64, 0, s>>>(D->mail.p, me, P, seq, D->err.p, timeout_ns);
+      k_account_mail<<<1, 32, 0, s>>>(R, D->mail.p, parity, ctx->run.p, ctx->high_water.p,
+                                      bytes_per_transfer);
+      launches += 4;
+      if (R.n) {
+        k_merge_mail<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(R, D->mail.p, parity,
+                                                                  p.visited.p, nwords);
+        ++launches;
+      }
+    }
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[4], s));
+    // commit: count pass, direction decision, write pass (as engine_bfs)
+    const uint32_t next_level = (uint32_t)(D->level + 1);
+    k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
+    ++launches;
+    if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
+    if (p.whi > p.wlo) launches += launch_commit_count(v, off, ctx->run.p, sms, s);
+    if (nwords - (p.whi - p.wlo) > 0) {
+      k_commit_rest<<<rest_grid, 256, 0, s>>>(v, next_level);
+      ++launches;
+    }
+    bool next_bu = ctx->direction == 2;
+    if (ctx->direction == 1) {
+      // Beamer's rule on this node's own rows: every node may pick its own
+      // phase-1 direction -- the discoveries (and levels) are the same.
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 3, &ctx->run.p->traversed_edges, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
+      BFB_CUDA(cudaStreamSynchronize(s));
+      const int64_t frontier = ctx->pinned[2], mf = ctx->pinned[1];
+      const double mu = (double)(p.owned_edges - ctx->pinned[3]);
+      next_bu = bottom_up;
+      if (!bottom_up && (double)mf > mu / ctx->do_alpha && frontier > prev_frontier)
+        next_bu = true;
+      else if (bottom_up && (double)frontier < (double)n / ctx->do_beta && frontier < prev_frontier)
+        next_bu = false;
+    }
+    if (p.whi > p.wlo) launches += launch_commit_write(v, off, next_level, !next_bu, sms, s);
+    if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
+    BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 4, D->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
+    BFB_CUDA(cudaGetLastError());
+    if (*(int32_t*)(ctx->pinned + 4))
+      return fail(BFB_ERR_CUDA, "peer barrier timed out (a rank stopped participating)");
+    if (ctx->timing) {
+      float a = 0, b = 0, c = 0;
+      BFB_CUDA(cudaEventElapsedTime(&a, D->ev[2], D->ev[3]));
+      BFB_CUDA(cudaEventElapsedTime(&b, D->ev[3], D->ev[4]));
+      BFB_CUDA(cudaEventElapsedTime(&c, D->ev[4], D->ev[5]));
+      t_expand += a;
+      t_exchange += b;
+      t_commit += c;
+    }
+    const int64_t f = ctx->pinned[2];
+    if (f == 0) break;
+    bottom_up = next_bu;
+    prev_frontier = f;
+    ++D->level;
+    ++D->levels;
+    D->reached += f;
+    ctx->last_sizes.push_back(f);
+    if (sizes_out && nsizes < max_levels) sizes_out[nsizes] = f;
+    ++nsizes;
+    if (D->level > n) return fail(BFB_ERR_CAPACITY, "level count exceeded |V| (internal error)");
+  }
+  D->launches += launches;
+  BFB_TRY(rank_finish(ctx, st));
+  RunCounters rc;
+  int64_t hw = 0;
+  BFB_CUDA(cudaMemcpy(&rc, ctx->run.p, sizeof(rc), cudaMemcpyDeviceToHost));
+  BFB_CUDA(cudaMemcpy(&hw, ctx->high_water.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (st) {
+    st->remote_messages = rc.remote_messages;
+    st->remote_vertices = rc.remote_vertices;
+    st->exchange_bytes = rc.exchange_bytes;
+    st->buffer_high_water_max = hw;
+    st->edges_examined = rc.edges_examined;
+    st->bottom_up_levels = bu_levels;
+    st->expand_ms = t_expand;
+    st->exchange_ms = t_exchange;
+    st->commit_ms = t_commit;
+    st->expand_launches = expand_launches;
+  }
+  if (hw > (int64_t)ctx->fanout * n && ctx->strategy == BFB_STRATEGY_BUTTERFLY)
+    return fail(BFB_ERR_CAPACITY, "buffer bound violated");
   return BFB_OK;
 }
 

@@ -405,6 +405,19 @@ int bfb_rank_finish(bfb_ctx* ctx, bfb_run_stats* stats_out) {
   return rank_finish(ctx, stats_out);
 }
 
+int bfb_rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
+                 bfb_run_stats* stats_out) {
+  CTX_GUARD(ctx);
+  if (max_levels < 0) return fail(BFB_ERR_INVALID, "bad argument");
+  return rank_bfs(ctx, root, sizes_out, max_levels, stats_out);
+}
+
+int bfb_rank_parents(bfb_ctx* ctx, int64_t* parents_out) {
+  CTX_GUARD(ctx);
+  if (!parents_out) return fail(BFB_ERR_INVALID, "null output");
+  return rank_parents(ctx, parents_out);
+}
+
 int bfb_rank_parents_raw(bfb_ctx* ctx, uint32_t* parents_out) {
   CTX_GUARD(ctx);
   if (!parents_out) return fail(BFB_ERR_INVALID, "null output");

@@ -246,7 +246,7 @@ class DeviceGraph:
         return out.tolist()
 
     def levels(self):
-        out = np.empty(self._n, dtype=np.uint32)
+        out = _POOL.array(self._n, np.uint32)
         check(_lib.load().bfb_copy_levels(self.handle, ptr(out, ctypes.c_uint32)))
         return out
 

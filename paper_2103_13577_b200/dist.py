@@ -23,6 +23,12 @@ one int64 per rank per round (barrier + sizes).  Snapshot buffers alternate by
 round parity, so one barrier per round suffices (a node re-uses a parity only
 after every peer has published the following round, which they do only after
 finishing the previous merge).
+
+``run_levels`` is the host-sequenced form of the protocol (one host round trip
+per round; it also drives the numpy test node of tests/).  ``RankEngine.run``
+uses the device-synchronised form by default (``bfb_rank_bfs``): the same
+rounds, with the barrier and the snapshot sizes exchanged through per-node
+mailboxes in HBM that peers write over NVLink, so a level costs one host sync.
 """
 
 from __future__ import annotations
@@ -135,13 +141,14 @@ class GpuNode:
         check(lib.bfb_rank_setup(dg.handle, b.size - 1, ptr(b, ctypes.c_int64), int(fanout),
                                  _lib.STRATEGY[strategy], 1 if parents else 0, self.rank))
         dg._engine_key = ("rank", tuple(b.tolist()), fanout, strategy, parents)
-        h = (ctypes.c_uint8 * 128)()
+        h = (ctypes.c_uint8 * 256)()
         check(lib.bfb_rank_ipc_handles(dg.handle, h))
         allh = comm.allgather_bytes(bytes(h))
         for peer, hb in enumerate(allh):
             if peer != self.rank:
-                buf = (ctypes.c_uint8 * 128).from_buffer_copy(hb)
+                buf = (ctypes.c_uint8 * 256).from_buffer_copy(hb)
                 check(lib.bfb_rank_open_peer(dg.handle, peer, buf))
+        comm.barrier()  # every peer mapped before any mailbox is written
         self.parents = parents
 
     def begin(self, root):
@@ -166,6 +173,16 @@ class GpuNode:
         check(_lib.load().bfb_rank_commit(self.dg.handle, byref(f), byref(o)))
         return f.value, o.value
 
+    def bfs(self, root, max_levels=4096):
+        """Whole BFS, device-synchronised (bfb_rank_bfs); returns (sizes, stats)."""
+        sizes = np.zeros(max_levels, dtype=np.int64)
+        st = _lib.RunStatsC()
+        check(_lib.load().bfb_rank_bfs(self.dg.handle, int(root), ptr(sizes, ctypes.c_int64),
+                                       max_levels, byref(st)))
+        if st.levels > max_levels:
+            raise RuntimeError("more levels than max_levels")
+        return sizes[:st.levels].tolist(), st
+
     def finish(self):
         st = _lib.RunStatsC()
         check(_lib.load().bfb_rank_finish(self.dg.handle, byref(st)))
@@ -173,6 +190,12 @@ class GpuNode:
 
     def levels(self):
         return self.dg.levels()
+
+    def output_parents(self):
+        """Output parents of the last device-synchronised BFS (peer HBM min)."""
+        out = np.empty(self.dg.num_vertices, dtype=np.int64)
+        check(_lib.load().bfb_rank_parents(self.dg.handle, ptr(out, ctypes.c_int64)))
+        return out
 
     def parents_raw(self):
         out = np.empty(self.dg.num_vertices, dtype=np.uint32)
@@ -184,8 +207,10 @@ class RankEngine:
     """engine.run for one rank of a torch.distributed job: every rank calls
     ``run(root)`` with the same root; each returns the same DistanceArray."""
 
-    def __init__(self, dg, boundaries, fanout=1, strategy="butterfly", parents=False, comm=None):
+    def __init__(self, dg, boundaries, fanout=1, strategy="butterfly", parents=False, comm=None,
+                 device_sync=True):
         self.comm = comm or Comm()
+        self.device_sync = device_sync
         n = len(boundaries) - 1
         if n != self.comm.size:
             raise ValueError("partition must have one part per rank")
@@ -195,16 +220,28 @@ class RankEngine:
         self.node = GpuNode(dg, boundaries, fanout, strategy, parents, self.comm)
         self.parents = parents
 
-    def run(self, root, levels=True):
-        sizes = run_levels(self.node, self.rounds, self.comm, root)
-        st = self.node.finish()
-        stats = aggregate_stats(self.comm, sizes, st)
+    def run(self, root, levels=True, parents=None):
+        """engine.run for this rank.  ``parents`` (default:
+        as set up) also assembles the output parents."""
+        parents = self.parents if parents is None else parents
+        if parents and not self.parents:
+            raise RuntimeError("engine set up without parents")
+        if self.device_sync:
+            sizes, st = self.node.bfs(root)
+        else:
+            sizes = run_levels(self.node, self.rounds, self.comm, root)
+            st = self.node.finish()
+        stats = aggregate_stats(self.comm, sizes, st)  # collective: every rank is done
         d = self.node.levels() if levels else None
         par = None
-        if self.parents and levels:
-            raw = self.node.parents_raw()
-            m = self.comm.allreduce_min_u32(raw)
-            par = np.where(m == 0xFFFFFFFF, -1, m).astype(np.int64)
+        if parents and levels:
+            if self.device_sync:
+                par = self.node.output_parents()  # min over the peers' parents, read over NVLink
+                self.comm.barrier()  # peers' parents stay intact until everyone has read
+            else:
+                raw = self.node.parents_raw()
+                m = self.comm.allreduce_min_u32(raw)
+                par = np.where(m == 0xFFFFFFFF, -1, m).astype(np.int64)
         return DistanceArray(d, int(root), par), stats
 
 
@@ -225,66 +262,3 @@ def aggregate_stats(comm, sizes, st):
         device_ms={"total": float(st.elapsed_ms)},
         kernel_launches=int(st.kernel_launches),
     )
-
-
-# ----------------------------------------------------------------- bench ---
-def bench_rank(args, cfg, metric, unit):
-    """bench.py at N > 1 under torchrun: one rank per GPU, s29 graph built on
-    every GPU (deterministic), node = rank, K timed BFS; time per BFS = max over
-    ranks of the device time; returns rank 0's JSON line."""
-    import time
-
-    import torch
-    import torch.distributed as dist
-
-    from . import graphs
-
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = int(os.environ.get("BFB_DEVICE", str(local)))
-    torch.cuda.set_device(dev)
-    if not dist.is_initialized():
-        backend = os.environ.get("BFB_DIST_BACKEND", "nccl")  # gloo: several ranks per GPU
-        if backend == "nccl":
-            dist.init_process_group(backend="nccl", device_id=torch.device("cuda", dev))
-        else:
-            dist.init_process_group(backend=backend)
-    comm = Comm()
-    P = comm.size
-    fanout = args.fanout or min(2, P)
-    parents = not args.no_parents
-    t0 = time.time()
-    g = graphs.kronecker(args.scale, args.edge_factor, 1, device=dev)
-    dg = g.device
-    build_s = time.time() - t0
-    b = dg.partition_1d(P)
-    roots = graphs.sample_roots(g, args.roots)
-    eng = RankEngine(dg, b, fanout, "butterfly", parents, comm)
-    K, W = args.steps, args.warmup
-    for i in range(W):
-        eng.run(int(roots[(K + i) % len(roots)]), levels=False)
-    comm.barrier()
-    teps, edges, tmax_all, launches = [], [], [], 0
-    dg.timer_start()
-    for i in range(K):
-        sizes = run_levels(eng.node, eng.rounds, comm, int(roots[i % len(roots)]))
-        st = eng.node.finish()
-        tmax = comm.allreduce(float(st.elapsed_ms), "max")
-        e = int(comm.allreduce(int(st.traversed_edges)))
-        teps.append(e / (tmax * 1e-3) / 1e9)
-        edges.append(e)
-        tmax_all.append(tmax)
-        launches += int(st.kernel_launches)
-    bracket = comm.allreduce(dg.timer_stop(), "max")
-    value = len(teps) / sum(1.0 / x for x in teps)
-    cfg = dict(cfg, fanout=fanout, num_parts=P)
-    line = {
-        "metric": metric, "value": round(value, 3), "unit": unit, "n_gpus": P, "steps": K,
-        "warmup": W, "ms_per_step": round(bracket / K, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": cfg, "aggregate_gteps": round(sum(edges) / (bracket * 1e-3) / 1e9, 3),
-        "graph": {"num_vertices": g.num_vertices, "num_edges": g.num_edges,
-                  "build_s": round(build_s, 2)},
-        "gpu_launches": launches,
-        "exchange": "CUDA-IPC peer snapshot reads fused with the OR-merge; gloo barrier+sizes",
-    }
-    return line if comm.rank == 0 else None
