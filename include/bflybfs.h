@@ -175,9 +175,9 @@ int bfb_probe_peak(bfb_ctx* ctx, int64_t bytes, int64_t* probes_out, double* ms_
 /* init's allocation step for node `rank` only (global partition boundaries). */
 int bfb_rank_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int fanout,
                    int strategy, int want_parents, int rank);
-/* 256 bytes: the IPC handles of this node's two (round-parity) snapshot
- * buffers, its mailbox (device-synchronised mode) and its parents (zero
- * without parents). */
+/* 320 bytes: the IPC handles of this node's two (round-parity) snapshot
+ * bitmaps, its mailbox and its queue-form snapshots (device-synchronised
+ * mode), and its parents (zero without parents). */
 int bfb_rank_ipc_handles(bfb_ctx* ctx, void* handles_out);
 int bfb_rank_open_peer(bfb_ctx* ctx, int peer, const void* handles);
 int bfb_rank_begin(bfb_ctx* ctx, int64_t root);

@@ -147,6 +147,7 @@ struct PartCounters {
   int64_t q_edges;      // sum of degrees over q_local
   int64_t frontier;     // |synchronized next frontier| counted at commit
   int64_t pub_count[2]; // published snapshot size, by round parity (phase 2)
+  int64_t pub_qpos[2];  // queue-form snapshot fill (device-synchronised mode)
 };
 
 // Device-resident run statistics (RunStats).
@@ -171,6 +172,7 @@ struct Part {
   DevBuf<uint32_t> parent;         // phase-1 parents (n) when wanted
   DevBuf<uint32_t> pub;            // published round snapshot (n bits)
   DevBuf<uint32_t> pub_alt;        // odd-round snapshot (multi-process mode)
+  DevBuf<uint32_t> pub_q;          // queue-form snapshots, 2 x nwords entries (by parity)
   DevBuf<uint32_t> front;          // level-L frontier bitmap (bottom-up phase 1)
   DevBuf<uint32_t> q_v;            // q_local vertex ids, ascending
   DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local

@@ -1016,6 +1016,7 @@ struct EngineTables {
   DevBuf<int32_t> err;
   std::vector<int64_t*> peer_mail;
   std::vector<uint32_t*> peer_parent;  // every node's phase-1 parents (IPC-mapped)
+  std::vector<const uint32_t*> peer_q; // every node's queue-form snapshots (IPC-mapped)
   int64_t seq = 0;
   int64_t level = 0, reached = 0, launches = 0, levels = 0;
   int64_t remote_messages = 0, remote_vertices = 0, high_water = 0, exchange_bytes = 0;
@@ -1502,6 +1503,7 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   for (int par = 0; par < 2; ++par) D->peer_pub[par].assign(parts, nullptr);
   D->peer_pub[0][rank] = p.pub.p;
   D->peer_pub[1][rank] = p.pub_alt.p;
+  BFB_TRY(p.pub_q.alloc(2 * (size_t)nwords_pad));
   BFB_TRY(D->mail.alloc(4 * (size_t)parts));
   BFB_CUDA(cudaMemset(D->mail.p, 0, 4 * (size_t)parts * sizeof(int64_t)));
   BFB_TRY(D->peer_mail_dev.alloc(parts));
@@ -1509,6 +1511,8 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   BFB_CUDA(cudaMemset(D->err.p, 0, sizeof(int32_t)));
   D->peer_mail.assign(parts, nullptr);
   D->peer_mail[rank] = D->mail.p;
+  D->peer_q.assign(parts, nullptr);
+  D->peer_q[rank] = p.pub_q.p;
   D->peer_parent.assign(parts, nullptr);
   if (want_parents) {
     D->peer_parent[rank] = p.parent.p;
@@ -1521,12 +1525,13 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
 
 int rank_ipc_handles(bfb_ctx* ctx, void* out) {
   if (!ctx->tables || ctx->tables->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
-  cudaIpcMemHandle_t h[4];
+  cudaIpcMemHandle_t h[5];
   std::memset(h, 0, sizeof(h));
   BFB_CUDA(cudaIpcGetMemHandle(&h[0], ctx->parts[0].pub.p));
   BFB_CUDA(cudaIpcGetMemHandle(&h[1], ctx->parts[0].pub_alt.p));
   BFB_CUDA(cudaIpcGetMemHandle(&h[2], ctx->tables->mail.p));
-  if (ctx->want_parents) BFB_CUDA(cudaIpcGetMemHandle(&h[3], ctx->parts[0].parent.p));
+  BFB_CUDA(cudaIpcGetMemHandle(&h[3], ctx->parts[0].pub_q.p));
+  if (ctx->want_parents) BFB_CUDA(cudaIpcGetMemHandle(&h[4], ctx->parts[0].parent.p));
   std::memcpy(out, h, sizeof(h));
   return BFB_OK;
 }
@@ -1536,9 +1541,9 @@ int rank_open_peer(bfb_ctx* ctx, int peer, const void* handles) {
   if (!D || D->rank < 0) return fail(BFB_ERR_STATE, "not in rank mode");
   if (peer < 0 || peer >= ctx->num_parts || peer == D->rank)
     return fail(BFB_ERR_INVALID, "bad peer");
-  cudaIpcMemHandle_t h[4];
+  cudaIpcMemHandle_t h[5];
   std::memcpy(h, handles, sizeof(h));
-  for (int k = 0; k < (ctx->want_parents ? 4 : 3); ++k) {
+  for (int k = 0; k < (ctx->want_parents ? 5 : 4); ++k) {
     void* ptr = nullptr;
     BFB_CUDA(cudaIpcOpenMemHandle(&ptr, h[k], cudaIpcMemLazyEnablePeerAccess));
     D->opened.push_back(ptr);
@@ -1546,6 +1551,8 @@ int rank_open_peer(bfb_ctx* ctx, int peer, const void* handles) {
       D->peer_pub[k][peer] = static_cast<const uint32_t*>(ptr);
     else if (k == 2)
       D->peer_mail[peer] = static_cast<int64_t*>(ptr);
+    else if (k == 3)
+      D->peer_q[peer] = static_cast<const uint32_t*>(ptr);
     else
       D->peer_parent[peer] = static_cast<uint32_t*>(ptr);
   }
@@ -1788,18 +1795,77 @@ __global__ void k_wait(const int64_t* mail, int me, int num_nodes, int64_t seq, 
 }
 
 struct RoundSrc {
-  const uint32_t* pub[kMaxSrc];
+  const uint32_t* pub[kMaxSrc];  // bitmap snapshot of this round's parity
+  const uint32_t* q[kMaxSrc];    // queue-form snapshot of this round's parity
   int id[kMaxSrc];
   int n;
 };
 
+// Publish for the device-synchronised mode: the round-start snapshot
+// visited & ~start as a bitmap (always) and, while it stays below qcap
+// entries, also as a vertex queue; a reader pulls whichever is smaller
+// (4 B per vertex vs n/8 B), so sparse rounds move only their vertices over
+// NVLink.  One atomic per warp reserves queue space.
+__global__ void __launch_bounds__(256) k_publish_q(PartView v, int parity, uint32_t* __restrict__ q,
+                                                   int64_t qcap) {
+  const int lane = threadIdx.x & 31;
+  int64_t cnt = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nw_round = (v.nwords + 31) & ~(int64_t)31;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw_round; w += stride) {
+    uint32_t p = 0;
+    if (w < v.nwords) {
+      p = v.visited[w] & ~v.start[w];
+      v.pub[w] = p;
+    }
+    const int c = __popc(p);
+    cnt += c;
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tot == 0) continue;
+    int64_t base = 0;
+    if (lane == 31) base = (int64_t)atomicAdd((unsigned long long*)&v.ctr->pub_qpos[parity],
+                                              (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    if (base + tot > qcap) continue;  // dense snapshot: readers use the bitmap
+    int64_t pos = base + incl - c;
+    for (uint32_t x = p; x; x &= x - 1) q[pos++] = (uint32_t)((w << 5) + __ffs(x) - 1);
+  }
+  __shared__ int64_t red[32];
+  cnt = block_sum_i64(cnt, red);
+  if (threadIdx.x == 0 && cnt)
+    atomicAdd((unsigned long long*)&v.ctr->pub_count[parity], (unsigned long long)cnt);
+}
+
+// Queue-form sources of a round: set each listed vertex's bit (several
+// sources and threads may hit one word, so atomically).
+__global__ void k_merge_queue(RoundSrc R, const int64_t* mail, int parity, int64_t qcap,
+                              uint32_t* __restrict__ vis) {
+  for (int i = 0; i < R.n; ++i) {
+    const int64_t k = mail[kMail * R.id[i] + parity];
+    if (k <= 0 || k > qcap) continue;
+    const uint32_t* __restrict__ q = R.q[i];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const uint32_t u = q[j];
+      const uint32_t bit = 1u << (u & 31);
+      if (!(vis[u >> 5] & bit)) atomicOr(&vis[u >> 5], bit);
+    }
+  }
+}
+
 // OR the non-empty sources' snapshots into visited (this node is the only
 // writer of its bitmap during the merge).
-__global__ void k_merge_mail(RoundSrc R, const int64_t* mail, int parity,
+__global__ void k_merge_mail(RoundSrc R, const int64_t* mail, int parity, int64_t qcap,
                              uint32_t* __restrict__ vis, int64_t nwords) {
-  uint64_t live = 0;
+  uint64_t live = 0;  // bitmap-form sources: non-empty and above the queue cap
   for (int i = 0; i < R.n; ++i)
-    if (mail[kMail * R.id[i] + parity] > 0) live |= 1ull << i;
+    if (mail[kMail * R.id[i] + parity] > qcap) live |= 1ull << i;
   if (!live) return;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -1814,19 +1880,20 @@ __global__ void k_merge_mail(RoundSrc R, const int64_t* mail, int parity,
 
 // RunStats accounting of one round from the mailbox sizes (one thread).
 __global__ void k_account_mail(RoundSrc R, const int64_t* mail, int parity, RunCounters* run,
-                               int64_t* hw, int64_t bytes_per_transfer) {
+                               int64_t* hw, int64_t bitmap_bytes, int64_t qcap) {
   if (threadIdx.x) return;
-  int64_t msgs = 0, in = 0;
+  int64_t msgs = 0, in = 0, bytes = 0;
   for (int i = 0; i < R.n; ++i) {
     const int64_t k = mail[kMail * R.id[i] + parity];
     if (k > 0) {
       ++msgs;
       in += k;
+      bytes += k <= qcap ? 4 * k : bitmap_bytes;
     }
   }
   run->remote_messages += msgs;
   run->remote_vertices += in;
-  run->exchange_bytes += msgs * bytes_per_transfer;
+  run->exchange_bytes += bytes;
   if (in > *hw) *hw = in;
 }
 
@@ -1849,6 +1916,8 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   const int sms = ctx->num_sms;
   const int64_t bytes_per_transfer = nwords * (int64_t)sizeof(uint32_t);
   const uint64_t timeout_ns = 60ull * 1000 * 1000 * 1000;
+  // queue-form snapshots pay off below n/32 vertices (4 B each vs n/8 B)
+  const int64_t qcap = (nwords + kWordPad - 1) / kWordPad * kWordPad + kWordPad;
   BFB_CUDA(cudaMemsetAsync(ctx->high_water.p, 0, sizeof(int64_t), s));
   std::vector<RoundSrc> rounds;
   for (auto& rnd : ctx->schedule) {
@@ -1889,18 +1958,25 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       const int parity = (int)(seq & 1);
       PartView pv = v;
       pv.pub = parity ? p.pub_alt.p : p.pub.p;
-      for (int i = 0; i < R.n; ++i) R.pub[i] = D->peer_pub[parity][R.id[i]];
+      for (int i = 0; i < R.n; ++i) {
+        R.pub[i] = D->peer_pub[parity][R.id[i]];
+        R.q[i] = D->peer_q[R.id[i]] + parity * qcap;
+      }
       BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_count[parity], 0, sizeof(int64_t), s));
-      k_publish<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(pv, parity);
+      BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_qpos[parity], 0, sizeof(int64_t), s));
+      k_publish_q<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(pv, parity,
+                                                                p.pub_q.p + parity * qcap, qcap);
       k_signal<<<1, 64, 0, s>>>(D->peer_mail_dev.p, me, P, seq, p.ctr.p, parity);
       k_wait<<<1, 64, 0, s>>>(D->mail.p, me, P, seq, D->err.p, timeout_ns);
       k_account_mail<<<1, 32, 0, s>>>(R, D->mail.p, parity, ctx->run.p, ctx->high_water.p,
-                                      bytes_per_transfer);
+                                      bytes_per_transfer, qcap);
       launches += 4;
       if (R.n) {
-        k_merge_mail<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(R, D->mail.p, parity,
+        k_merge_queue<<<grid_cap(qcap, 256, sms, 2), 256, 0, s>>>(R, D->mail.p, parity, qcap,
+                                                                   p.visited.p);
+        k_merge_mail<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(R, D->mail.p, parity, qcap,
                                                                   p.visited.p, nwords);
-        ++launches;
+        launches += 2;
       }
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[4], s));

@@ -141,12 +141,12 @@ class GpuNode:
         check(lib.bfb_rank_setup(dg.handle, b.size - 1, ptr(b, ctypes.c_int64), int(fanout),
                                  _lib.STRATEGY[strategy], 1 if parents else 0, self.rank))
         dg._engine_key = ("rank", tuple(b.tolist()), fanout, strategy, parents)
-        h = (ctypes.c_uint8 * 256)()
+        h = (ctypes.c_uint8 * 320)()
         check(lib.bfb_rank_ipc_handles(dg.handle, h))
         allh = comm.allgather_bytes(bytes(h))
         for peer, hb in enumerate(allh):
             if peer != self.rank:
-                buf = (ctypes.c_uint8 * 256).from_buffer_copy(hb)
+                buf = (ctypes.c_uint8 * 320).from_buffer_copy(hb)
                 check(lib.bfb_rank_open_peer(dg.handle, peer, buf))
         comm.barrier()  # every peer mapped before any mailbox is written
         self.parents = parents
