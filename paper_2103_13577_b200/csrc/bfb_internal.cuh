@@ -137,6 +137,7 @@ struct DevGraph {
   int64_t n = 0, m = 0, max_degree = 0;
   DevBuf<int64_t> offsets;   // n+1
   DevBuf<uint32_t> adj;      // m
+  DevBuf<uint32_t> nonisol;  // bitmap of degree > 0 (bottom-up candidates), built at engine setup
   bool valid = false;
 };
 

@@ -55,8 +55,10 @@ struct PartView {
   int64_t abase, nunits;  // commit units: words [abase, abase + 32 * nunits)
   uint32_t* ucnt;
   int64_t *udeg, *upos, *uepre, *tcnt, *tdeg;
+  bool rebuild;  // commit passes: new vertices = the frontier bitmap (queue rebuild)
   PartCounters* ctr;
   const int64_t* off;  // CSR offsets (rows of q_v)
+  const uint32_t* nonisol;  // degree > 0 bitmap
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
@@ -86,8 +88,10 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.uepre = v.upos + nu;
   v.tcnt = v.uepre + nu;
   v.tdeg = v.tcnt + nt;
+  v.rebuild = false;
   v.ctr = p.ctr.p;
   v.off = ctx->g.offsets.p;
+  v.nonisol = ctx->g.nonisol.p;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -566,7 +570,10 @@ __device__ __forceinline__ void unit_word(const PartView& v, int64_t unit, int l
   const int64_t w = v.abase + unit * 32 + lane;
   const bool in = w >= v.wlo && w < v.whi;
   a = in ? v.visited[w] : 0u;
-  nb = a & ~(in ? v.start[w] : 0u);
+  if (v.rebuild)
+    nb = in ? v.front[w] : 0u;  // this level's new vertices, already committed
+  else
+    nb = a & ~(in ? v.start[w] : 0u);
   own = nb & owned_mask(w, v.lo, v.hi);
 }
 
@@ -589,7 +596,7 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
   for (int64_t unit = gw; unit < v.nunits; unit += nw) {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
-    fr += __popc(nb);
+    if (!v.rebuild) fr += __popc(nb);  // a rebuild's frontier was counted by its level's commit
     const uint32_t c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(own));
     int64_t d = 0;
     if (c) d = warp_sum_i64(word_degree_sum(own, (v.abase + unit * 32 + lane) << 5, off));
@@ -653,7 +660,7 @@ __global__ void __launch_bounds__(1024) k_unit_scan_tiles(PartView v, int64_t nt
   if (threadIdx.x == 0) {
     v.ctr->q_count = carry_c;
     v.ctr->q_edges = carry_d;
-    atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)carry_d);
+    if (!v.rebuild) atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)carry_d);
   }
 }
 
@@ -709,7 +716,7 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
     unsigned m = __ballot_sync(0xffffffffu, nb != 0);
     if (!m) continue;
     const int64_t w0 = v.abase + unit * 32;
-    while (m) {
+    while (m && !v.rebuild) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
@@ -757,9 +764,59 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
       ecarry += __shfl_sync(0xffffffffu, inc, 31);
     }
     __syncwarp();
+    if (nb && !v.rebuild) {
+      v.start[w0 + lane] = a;
+      if (v.front) v.front[w0 + lane] = nb;
+    }
+  }
+}
+
+// Queue-less commit of a bottom-up level in one pass (the next phase 1 is
+// bottom-up again, which reads only bitmaps): per 32-word unit, levels of the
+// new vertices (lane = bit, coalesced), start := visited, the frontier
+// bitmap, and the totals -- frontier, owned new vertices and their degree sum
+// (q_count / q_edges for the direction heuristic, RunStats traversed edges).
+// If the heuristic then switches to top-down, the queue is rebuilt from the
+// frontier bitmap by the regular count -> scan -> write passes (PartView
+// rebuild).
+__global__ void __launch_bounds__(256) k_commit_light_count(PartView v, const int64_t* __restrict__ off,
+                                                            uint32_t next_level, RunCounters* run) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t fr = 0, qc = 0, qe = 0;
+  for (int64_t unit = gw; unit < v.nunits; unit += nw) {
+    uint32_t a, nb, own;
+    unit_word(v, unit, lane, a, nb, own);
+    unsigned m = __ballot_sync(0xffffffffu, nb != 0);
+    if (!m) continue;
+    const int64_t w0 = v.abase + unit * 32;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
+      if ((x >> lane) & 1u) v.level[((w0 + j) << 5) + lane] = next_level;
+    }
     if (nb) {
       v.start[w0 + lane] = a;
       if (v.front) v.front[w0 + lane] = nb;
+      fr += __popc(nb);
+    }
+    if (own) {
+      qc += __popc(own);
+      qe += word_degree_sum(own, (w0 + lane) << 5, off);
+    }
+  }
+  __shared__ int64_t red[32];
+  fr = block_sum_i64(fr, red);
+  qc = block_sum_i64(qc, red);
+  qe = block_sum_i64(qe, red);
+  if (threadIdx.x == 0) {
+    if (fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+    if (qc) atomicAdd((unsigned long long*)&v.ctr->q_count, (unsigned long long)qc);
+    if (qe) {
+      atomicAdd((unsigned long long*)&v.ctr->q_edges, (unsigned long long)qe);
+      atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)qe);
     }
   }
 }
@@ -834,7 +891,7 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
   unsigned long long ex = 0;
   for (int64_t w = v.wlo + gw; w < v.whi; w += nw) {
     const uint32_t vis = v.visited[w];
-    const uint32_t cand = owned_mask(w, v.lo, v.hi) & ~vis;
+    const uint32_t cand = owned_mask(w, v.lo, v.hi) & ~vis & v.nonisol[w];
     if (!cand) continue;
     const int64_t u = (w << 5) + lane;
     bool found = false;
@@ -876,6 +933,19 @@ __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n
     uint32_t best = kNone;
     for (int g = 0; g < num_nodes; ++g) best = min(best, parents[g][i]);
     out[i] = best;
+  }
+}
+
+// Bitmap of vertices with degree > 0 (lane = vertex, ballot per word).
+__global__ void k_nonisolated(const int64_t* __restrict__ off, int64_t n, uint32_t* out,
+                              int64_t nwords_pad) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords_pad;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t u = (w << 5) + lane;
+    const bool has = u < n && __ldg(off + u + 1) > __ldg(off + u);
+    const unsigned b = __ballot_sync(0xffffffffu, has);
+    if (lane == 0) out[w] = b;
   }
 }
 
@@ -987,6 +1057,21 @@ int launch_commit_write(const PartView& v, const int64_t* off, uint32_t next_lev
   return 2;
 }
 
+// Bottom-up level commit (one pass); rebuild: the queue for a following
+// top-down level, from the frontier bitmap, by count -> scan -> write.
+int launch_commit_light_count(const PartView& v, const int64_t* off, uint32_t next_level,
+                              RunCounters* run, int sms, cudaStream_t s) {
+  k_commit_light_count<<<grid_cap(v.nunits * 32, 256, sms, 8), 256, 0, s>>>(v, off, next_level, run);
+  return 1;
+}
+
+int launch_commit_rebuild(PartView v, const int64_t* off, uint32_t next_level, RunCounters* run,
+                          int sms, cudaStream_t s) {
+  v.rebuild = true;
+  return launch_commit_count(v, off, run, sms, s) +
+         launch_commit_write(v, off, next_level, true, sms, s);
+}
+
 int launch_commit(const PartView& v, const int64_t* off, uint32_t next_level, RunCounters* run,
                   int sms, cudaStream_t s) {
   return launch_commit_count(v, off, run, sms, s) +
@@ -1095,6 +1180,10 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
       BFB_CUDA(cudaMemcpy(&off_h[g], ctx->g.offsets.p + bounds[g], sizeof(int64_t),
                           cudaMemcpyDeviceToHost));
   }
+  BFB_TRY(ctx->g.nonisol.alloc(nwords_pad));
+  k_nonisolated<<<grid_cap(nwords_pad * 32, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
+      ctx->g.offsets.p, n, ctx->g.nonisol.p, nwords_pad);
+  BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->parts.resize(parts);
   std::vector<uint32_t*> pubs(parts), viss(parts), pars(parts);
   std::vector<PartCounters*> ctrs(parts);
@@ -1296,10 +1385,19 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     if (ctx->direction)
       for (int g = 0; g < P; ++g)
         BFB_CUDA(cudaMemsetAsync(ctx->parts[g].front.p, 0, nwords * sizeof(uint32_t), s));
+    // Top-down level: count, [decide,] write with or without the queue.
+    // Bottom-up level: one queue-less pass; the queue is rebuilt from the
+    // frontier bitmap only on the switch back to top-down.
+    const bool light = ctx->direction != 0 && bottom_up;
     for (int g = 0; g < P; ++g) {
       Part& p = ctx->parts[g];
       PartView v = view_of(ctx, p);
-      if (p.whi > p.wlo) launches += launch_commit_count(v, off, ctx->run.p, sms, s);
+      if (p.whi > p.wlo) {
+        if (light)
+          launches += launch_commit_light_count(v, off, next_level, ctx->run.p, sms, s);
+        else
+          launches += launch_commit_count(v, off, ctx->run.p, sms, s);
+      }
       if (nwords - (p.whi - p.wlo) > 0) {
         k_commit_rest<<<small_grid, 256, 0, s>>>(v, next_level);
         ++launches;
@@ -1333,8 +1431,13 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     }
     for (int g = 0; g < P; ++g) {
       Part& p = ctx->parts[g];
-      if (p.whi > p.wlo)
+      if (p.whi <= p.wlo) continue;
+      if (light) {
+        if (!next_bu)
+          launches += launch_commit_rebuild(view_of(ctx, p), off, next_level, ctx->run.p, sms, s);
+      } else {
         launches += launch_commit_write(view_of(ctx, p), off, next_level, !next_bu, sms, s);
+      }
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
     if (frontier < 0)
@@ -1985,7 +2088,13 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
     ++launches;
     if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
-    if (p.whi > p.wlo) launches += launch_commit_count(v, off, ctx->run.p, sms, s);
+    const bool light = ctx->direction != 0 && bottom_up;
+    if (p.whi > p.wlo) {
+      if (light)
+        launches += launch_commit_light_count(v, off, next_level, ctx->run.p, sms, s);
+      else
+        launches += launch_commit_count(v, off, ctx->run.p, sms, s);
+    }
     if (nwords - (p.whi - p.wlo) > 0) {
       k_commit_rest<<<rest_grid, 256, 0, s>>>(v, next_level);
       ++launches;
@@ -2006,7 +2115,14 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       else if (bottom_up && (double)frontier < (double)n / ctx->do_beta && frontier < prev_frontier)
         next_bu = false;
     }
-    if (p.whi > p.wlo) launches += launch_commit_write(v, off, next_level, !next_bu, sms, s);
+    if (p.whi > p.wlo) {
+      if (light) {
+        if (!next_bu)
+          launches += launch_commit_rebuild(v, off, next_level, ctx->run.p, sms, s);
+      } else {
+        launches += launch_commit_write(v, off, next_level, !next_bu, sms, s);
+      }
+    }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 4, D->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

@@ -15,7 +15,7 @@ dg = g.device
 roots = graphs.sample_roots(g, 6)
 for parents, direction in ((False, "top-down"), (True, "top-down"), (True, "optimizing"), (False, "optimizing")):
     dg.setup(dg.partition_1d(1), 1, "butterfly", parents=parents)
-    dg.set_direction(direction)
+    dg.set_direction(direction, float(os.environ.get("SW_ALPHA", "14")), float(os.environ.get("SW_BETA", "24")))
     dg.set_timing(True)
     dg.bfs(int(roots[0]), levels=False)
     t = []; ex = []; cm = []
