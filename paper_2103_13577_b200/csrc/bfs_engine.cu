@@ -30,11 +30,10 @@ namespace bfb {
 namespace {
 
 constexpr int kExpandBlock = 256;
-#ifndef BFB_EXPAND_ITEMS
-#define BFB_EXPAND_ITEMS 8
-#endif
-constexpr int kExpandItems = BFB_EXPAND_ITEMS;
-constexpr int64_t kTile = (int64_t)kExpandBlock * kExpandItems;  // edges per tile
+constexpr int kExpandItems = 8;                // edges per lane per subtile
+constexpr int64_t kSub = 32 * kExpandItems;     // edges per subtile (one warp pass)
+constexpr int kSubPerTile = 8;
+constexpr int64_t kTile = kSub * kSubPerTile;   // edges per tile (tile_vstart granularity)
 constexpr int kScanItems = 16;                 // commit unit scan: units per thread
 constexpr int64_t kScanTile = 256 * kScanItems;
 constexpr int64_t kWordPad = 1024;  // bitmap allocation padding (words)
@@ -127,232 +126,131 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
 }
 
 // ------------------------------------------------------------ phase 1 ----
-// Phase 1: edge-balanced top-down expansion of q_local.
-// The frontier's edges are cut into 2048-edge tiles (load-balanced search
-// over the degree prefix q_pre); blocks stride over tiles.  Per edge: the
-// adjacency word, a probe of the visited bitmap and, when the probe finds the
-// bit clear, a fire-and-forget red.or claim (check-and-set) --
-// the commit finds the new bits as visited & ~start, so no claim needs the
-// atomic's old value.
-//
-// Software pipeline, one tile deep: while the probes of tile t are in flight
-// the block stages tile t+grid -- resolves each edge's row (from registers
-// for hub tiles of at most kRegSegs rows, else from a shared-memory owner
-// map) and issues cp.async copies of its adjacency words into the other half
-// of a double-buffered shared ring.  Each thread copies and later reads the
-// same ring slots, so the ring needs no block barrier; the adjacency HBM
-// latency and the row-resolution latency both overlap the probe latency.
-//
-// Parents: every claimant whose probe saw the bit clear stores its row
-// vertex as u's parent (plain store, last writer wins).  Every such writer is
-// a level-L vertex adjacent to u and u is discovered at level L+1 (bits set
-// before the launch are never seen clear), so whichever store lands is a
-// valid BFS parent -- no atomic with return on the critical path.
-constexpr int kRegSegs = 4;
+// Phase 1: top-down expansion of q_local, warp-centric.
+// The frontier's edges (degree prefix q_pre over q_local) are cut into
+// 2048-edge tiles; tile_vstart[t] is the row holding tile t's first edge
+// (written by the commit).  A warp works through a tile in 256-edge
+// subtiles, 8 edges per lane, lane-interleaved so the adjacency loads
+// coalesce, and resolves each edge's row in registers -- no shared memory, no
+// block barriers:
+//   lane j loads row rb+j's degree prefix and adjacency base (q_pre, q_base);
+//   the starts of rows rb+1..rb+30 inside the subtile become eight 32-bit
+//   masks (one warp OR-reduction per 32 positions); an edge's row is rb + the
+//   number of row starts at or before it (popc), its base comes from that
+//   row's lane by shuffle.  A subtile spanning more than 31 rows (average
+//   degree < 8) takes further batches of 31 rows.  Every reached vertex other
+//   than an isolated root has degree >= 1, so row starts are distinct.
+// Dense levels: one warp per tile, subtiles in order, the row cursor carried.
+// Sparse levels (fewer tiles than warps): one warp per subtile, its first
+// row found by a 32-ary warp search of q_pre inside the tile's rows, so a
+// small frontier still spreads over many warps.
+// Per edge: the adjacency word (evict-first), a probe of the visited bitmap
+// and, if the probe saw the bit clear, a fire-and-forget red.or claim
+// (check-and-set).  The commit finds the new bits as
+// visited & ~start, so no claim needs the atomic's old value.
+// Parents: every claimant whose probe saw the bit clear stores its row vertex
+// as u's parent (plain store, last writer wins).  Each such writer is a
+// level-L vertex adjacent to u, and u is discovered at level L+1 (bits set
+// before the launch are never seen clear), so any store that lands is a valid
+// BFS parent -- no atomic with return on the critical path.
 #ifndef BFB_EXPAND_MINB
 #define BFB_EXPAND_MINB 4
 #endif
-constexpr int kExpandMinBlocks = BFB_EXPAND_MINB;  // 4 blocks, 32 warps per SM
 
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-
-// 4-byte async global -> shared copy; the adjacency is read once per BFS, so
-// it is marked evict-first in L2 (the visited bitmap stays resident).
-__device__ __forceinline__ void cp_async_u32(uint32_t* dst, const uint32_t* src, uint64_t pol) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
+// One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
+// with rb the row holding edge r0 and ve the last row that can matter.
+// Returns the row holding edge r0 + kSub (the next subtile's cursor).
 template <bool kParents>
-struct ExpandSmem {
-  static constexpr int kP = kParents ? kTile : 1;
-  int64_t base[kTile + 1];       // per row: adjacency index - edge prefix (q_base)
-  uint32_t ring[2][kTile];       // adjacency words of the tile in flight / being staged
-  uint32_t ring_src[2][kP];      // parents: row vertex per edge (thread-private slots)
-  int32_t own[kTile];            // owner map: edge -> row within the tile
-  uint32_t rowv[kP + 1];         // per row: vertex id (parents)
-  int32_t wmax[kExpandBlock / 32];
-};
-
-// Stage tile t into ring slot `slot`: resolve rows, issue the cp.async copies,
-// record row vertices for parents.  Block-uniform (uses __syncthreads on the
-// owner-map path).  Returns the tile's edge count.
-template <bool kParents>
-__device__ __forceinline__ int stage_tile(const PartView& v, const uint32_t* __restrict__ adj,
-                                          ExpandSmem<kParents>& S, int slot, int64_t t, int64_t ntiles,
-                                          int64_t T, int64_t qc, int32_t& tag, uint64_t pol) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t e0 = t * kTile;
-  const int span = (int)min((int64_t)kTile, T - e0);
-  const int64_t vs = v.tile_vstart[t];
-  const int64_t ve = (t + 1 < ntiles) ? (int64_t)v.tile_vstart[t + 1] : qc - 1;
-  const int nseg = (int)(ve - vs + 1);
-  uint32_t* ring = S.ring[slot];
-  if (nseg <= kRegSegs) {
-    int32_t rel[kRegSegs];
-    int64_t base[kRegSegs];
-    uint32_t sv[kRegSegs];
-#pragma unroll
-    for (int k = 0; k < kRegSegs; ++k) {
-      rel[k] = INT32_MAX;
-      base[k] = 0;
-      sv[k] = 0;
-      if (k < nseg) {
-        const int64_t pre = __ldg(v.q_pre + vs + k);
-        rel[k] = (int32_t)max(pre - e0, (int64_t)INT32_MIN);
-        base[k] = __ldg(v.q_base + vs + k);
-        if (kParents) sv[k] = __ldg(v.q_v + vs + k);
-      }
-    }
+__device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
+                                                   const uint32_t* __restrict__ adj, int64_t r0,
+                                                   int span, uint32_t rb, uint32_t ve,
+                                                   unsigned le_mask) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t vs = rb;
+  uint32_t u[kExpandItems];
+  uint32_t rows[kExpandItems / 2];  // parents: row - vs, 16 bits per item
+  unsigned done = 0;                // items whose row is resolved
+  int lo = 0;                       // first position this batch covers
+  uint32_t next = rb;
+  while (true) {
+    const uint32_t row = rb + lane;
+    const bool valid = row <= ve;
+    const int64_t pre = valid ? __ldg(v.q_pre + row) : INT64_MAX;
+    const int64_t base = valid ? __ldg(v.q_base + row) : 0;
+    const int64_t relw = pre - r0;
+    const int rel = relw > kSub ? (int)kSub + 1 : (int)relw;  // row start, subtile-relative
+    const int hi = __shfl_sync(0xffffffffu, rel, 31);        // rows rb..rb+30 end here
+    const int cover_hi = min(hi, span);
+    const bool mine = lane >= 1 && lane <= 30 && rel > lo && rel < (int)kSub;
+    unsigned before = 0;
 #pragma unroll
     for (int it = 0; it < kExpandItems; ++it) {
-      const int r = it * kExpandBlock + threadIdx.x;
-      if (r < span) {
-        int64_t b = base[0];
-        uint32_t s0 = sv[0];
-#pragma unroll
-        for (int k = 1; k < kRegSegs; ++k)
-          if (r >= rel[k]) {
-            b = base[k];
-            s0 = sv[k];
-          }
-        cp_async_u32(ring + r, adj + b + e0 + r, pol);
-        if (kParents) S.ring_src[slot][r] = s0;
+      const unsigned M =
+          __reduce_or_sync(0xffffffffu, (mine && (rel >> 5) == it) ? (1u << (rel & 31)) : 0u);
+      const int r = it * 32 + lane;
+      const int idx = (int)before + __popc(M & le_mask);
+      before += __popc(M);
+      const int64_t b = __shfl_sync(0xffffffffu, base, idx);
+      if (r >= lo && r < cover_hi) {
+        u[it] = ld_stream_u32(adj + b + r0 + r);
+        done |= 1u << it;
+        if (kParents) {
+          const uint32_t ro = rb + idx - vs;
+          rows[it >> 1] = (it & 1) ? ((rows[it >> 1] & 0xFFFFu) | (ro << 16))
+                                   : ((rows[it >> 1] & 0xFFFF0000u) | ro);
+        }
       }
     }
-    cp_async_commit();
-    return span;
-  }
-  // Owner map: row starts scattered with a per-tile tag in the high bits, so
-  // the block max-scan ignores entries left by earlier tiles (no reset).
-  __syncthreads();  // every thread is done reading the previous map
-  ++tag;
-  const int32_t tg = tag << 12;
-  if (threadIdx.x == 0) S.own[0] = tg;
-  for (int k = threadIdx.x; k < nseg; k += kExpandBlock) {
-    const int64_t pre = v.q_pre[vs + k];
-    S.base[k] = v.q_base[vs + k];
-    if (kParents) S.rowv[k] = v.q_v[vs + k];
-    const int64_t r = pre - e0;
-    if (r > 0 && r < span) S.own[r] = tg | k;
-  }
-  __syncthreads();
-  {  // inclusive max-scan of the owner map, kTile / kExpandBlock entries per thread
-    constexpr int kPer = kTile / kExpandBlock;
-    int32_t loc[kPer];
-    int32_t run = 0;
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      run = max(run, S.own[threadIdx.x * kPer + i]);
-      loc[i] = run;
+    if (hi >= span) {
+      // the next subtile starts in the row holding position kSub
+      const unsigned last = __ballot_sync(0xffffffffu, rel <= (int)kSub && rel > lo);
+      next = rb + (31 - __clz((int)(last | 1u)));
+      break;
     }
-    int32_t inc = run;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= d) inc = max(inc, o);
-    }
-    if (lane == 31) S.wmax[warp] = inc;
-    __syncthreads();
-    int32_t carry = 0;
-    for (int w = 0; w < warp; ++w) carry = max(carry, S.wmax[w]);
-    const int32_t up = __shfl_up_sync(0xffffffffu, inc, 1);
-    const int32_t prev = max(carry, lane > 0 ? up : 0);
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) S.own[threadIdx.x * kPer + i] = max(prev, loc[i]) & 0xFFF;
-    __syncthreads();
+    rb += 31;
+    lo = hi;
   }
+  uint32_t* __restrict__ visited = v.visited;
+  uint32_t wv[kExpandItems];
+#pragma unroll
+  for (int it = 0; it < kExpandItems; ++it)
+    wv[it] = ((done >> it) & 1u) ? visited[u[it] >> 5] : 0xFFFFFFFFu;
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
-    const int r = it * kExpandBlock + threadIdx.x;
-    if (r < span) {
-      const int sg = S.own[r];
-      cp_async_u32(ring + r, adj + S.base[sg] + e0 + r, pol);
-      if (kParents) S.ring_src[slot][r] = S.rowv[sg];
-    }
-  }
-  cp_async_commit();
-  return span;
-}
-
-template <bool kParents>
-__global__ void __launch_bounds__(kExpandBlock, kExpandMinBlocks) k_expand(PartView v,
-                                                         const uint32_t* __restrict__ adj) {
-  extern __shared__ __align__(16) unsigned char expand_smem[];
-  ExpandSmem<kParents>& S = *reinterpret_cast<ExpandSmem<kParents>*>(expand_smem);
-  const int64_t T = v.ctr->q_edges;
-  if (T == 0) return;
-  const int64_t qc = v.ctr->q_count;
-  const int64_t ntiles = (T + kTile - 1) / kTile;
-  int64_t t = blockIdx.x;
-  if (t >= ntiles) return;
-  uint32_t* __restrict__ visited = v.visited;
-  uint32_t* __restrict__ parent = v.parent;
-  const uint64_t pol = l2_evict_first_policy();
-  int32_t tag = 0;
-  for (int k = threadIdx.x; k < kTile; k += kExpandBlock) S.own[k] = 0;
-  int slot = 0;
-  int span = stage_tile<kParents>(v, adj, S, 0, t, ntiles, T, qc, tag, pol);
-  for (; t < ntiles; t += gridDim.x) {
-    cp_async_wait_all();  // this thread's copies of tile t have landed
-    const uint32_t* ring = S.ring[slot];
-    uint32_t u[kExpandItems], wv[kExpandItems];
-#pragma unroll
-    for (int it = 0; it < kExpandItems; ++it) {
-      const int r = it * kExpandBlock + threadIdx.x;
-      u[it] = r < span ? ring[r] : 0u;
-      wv[it] = r < span ? visited[u[it] >> 5] : 0xFFFFFFFFu;
-    }
-    // stage the next tile while the probes are in flight
-    const int64_t tn = t + gridDim.x;
-    const int span_next =
-        tn < ntiles ? stage_tile<kParents>(v, adj, S, slot ^ 1, tn, ntiles, T, qc, tag, pol) : 0;
-#pragma unroll
-    for (int it = 0; it < kExpandItems; ++it) {
-      const uint32_t bit = 1u << (u[it] & 31);
-      if (!(wv[it] & bit)) {
-        atomicOr(&visited[u[it] >> 5], bit);
-        if (kParents) parent[u[it]] = S.ring_src[slot][it * kExpandBlock + threadIdx.x];
+    const uint32_t bit = 1u << (u[it] & 31);
+    if (!(wv[it] & bit)) {
+      atomicOr(&visited[u[it] >> 5], bit);
+      if (kParents) {
+        const uint32_t ro = (rows[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
+        v.parent[u[it]] = __ldg(v.q_v + vs + ro);
       }
     }
-    span = span_next;
-    slot ^= 1;
   }
+  return next;
+}
+
+// Row of q_local rows [lo, hi] holding edge position `pos` (the last row whose
+// degree prefix is <= pos): 32-ary warp search, 3 steps for a 2048-edge tile.
+__device__ __forceinline__ uint32_t find_row(const int64_t* __restrict__ q_pre, uint32_t lo,
+                                             uint32_t hi, int64_t pos) {
+  const int lane = threadIdx.x & 31;
+  while (hi > lo) {
+    const uint32_t span = hi - lo;  // answer in [lo, hi]
+    const uint32_t step = span / 32 + 1;  // 32 probes cover the span + 1 rows
+    const uint32_t cand = lo + (uint32_t)lane * step;
+    const bool le = cand <= hi && (lane == 0 || __ldg(q_pre + cand) <= pos);
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    const int k = 31 - __clz((int)m);  // last probe at or before pos (lane 0 always)
+    const uint32_t nlo = lo + (uint32_t)k * step;
+    const uint32_t nhi = min(hi, nlo + step - 1);
+    lo = nlo;
+    hi = step == 1 ? nlo : nhi;
+  }
+  return lo;
 }
 
 template <bool kParents>
-constexpr size_t expand_smem_bytes() { return sizeof(ExpandSmem<kParents>); }
-
-// Warp-centric phase 1: one warp per 2048-edge tile, in 8 rounds of 256
-// edges (8 per lane, lane-interleaved so adjacency loads coalesce).  No
-// shared memory and no block barriers: each round resolves its edges' rows
-// in registers.  Lane j loads row rb+j of the frontier queue (its degree
-// prefix, adjacency base and vertex); the starts of rows rb+1..rb+30 that fall
-// inside the round become bits of eight 32-bit masks (one warp OR-reduction
-// per 32 positions); an edge's row is rb + the number of row starts at or
-// before it (popc), and its base comes from that row's lane by shuffle.  A
-// round spanning more than 31 rows (average degree < 8) takes further
-// batches of 31 rows.  Every reached vertex other than an isolated root has
-// degree >= 1, so row starts are distinct.
-#ifndef BFB_EXPAND_DEFER
-#define BFB_EXPAND_DEFER 0  // 1: resolve all rows of a round first, then issue its loads
-#endif
-#ifndef BFB_EXPAND_WARP_MINB
-#define BFB_EXPAND_WARP_MINB 4
-#endif
-constexpr int kRound = 256;                      // edges per warp round
-constexpr int kRoundsPerTile = (int)(kTile / kRound);
-
-template <bool kParents>
-__global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_WARP_MINB)
+__global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
     k_expand_w(PartView v, const uint32_t* __restrict__ adj) {
   const int64_t T = v.ctr->q_edges;
   if (T == 0) return;
@@ -360,112 +258,40 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_WARP_MINB)
   const int64_t ntiles = (T + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31;
   const unsigned le_mask = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // bits [0, lane]
-  uint32_t* __restrict__ visited = v.visited;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += nwarps) {
-    const int64_t e0 = t * kTile;
-    const int span = (int)min((int64_t)kTile, T - e0);
-    const uint32_t vs = v.tile_vstart[t];
-    const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
-    uint32_t cur = vs;  // row containing the round's first edge
-    for (int rd = 0; rd * kRound < span; ++rd) {
-      const int64_t r0 = e0 + rd * kRound;  // global edge index of position 0
-      const int rspan = min(kRound, span - rd * kRound);
-      uint32_t u[kExpandItems];
-#if BFB_EXPAND_DEFER
-      int64_t addr[kExpandItems];
-#endif
-      uint32_t rows[kExpandItems / 2];  // parents: row - vs, 16 bits per item
-      unsigned done = 0;                // items whose row is resolved
-      uint32_t rb = cur;
-      int lo = 0;  // first position this batch covers
-      while (true) {
-        const uint32_t row = rb + lane;
-        const bool valid = row <= ve;
-        const int64_t pre = valid ? __ldg(v.q_pre + row) : INT64_MAX;
-        const int64_t base = valid ? __ldg(v.q_base + row) : 0;
-        const int64_t relw = pre - r0;
-        const int rel = relw > kRound ? kRound + 1 : (int)relw;  // row start, round-relative
-        const int hi = __shfl_sync(0xffffffffu, rel, 31);       // rows rb..rb+30 end here
-        const int cover_hi = min(min(hi, kRound), rspan);
-        const bool mine = lane >= 1 && lane <= 30 && rel > lo && rel < kRound;
-        unsigned before = 0;
-#pragma unroll
-        for (int it = 0; it < kExpandItems; ++it) {
-          const unsigned M = __reduce_or_sync(0xffffffffu, (mine && (rel >> 5) == it) ? (1u << (rel & 31)) : 0u);
-          const int r = it * 32 + lane;
-          const int idx = (int)before + __popc(M & le_mask);
-          before += __popc(M);
-          const int64_t b = __shfl_sync(0xffffffffu, base, idx);
-          if (r >= lo && r < cover_hi) {
-#if BFB_EXPAND_DEFER
-            addr[it] = b + r0 + r;
-#else
-            u[it] = ld_stream_u32(adj + b + r0 + r);
-#endif
-            done |= 1u << it;
-            if (kParents) {
-              const uint32_t ro = rb + idx - vs;
-              rows[it >> 1] = (it & 1) ? ((rows[it >> 1] & 0xFFFFu) | (ro << 16))
-                                       : ((rows[it >> 1] & 0xFFFF0000u) | ro);
-            }
-          }
-        }
-        if (hi >= rspan) {
-          // next round starts in the row containing position kRound
-          const unsigned last = __ballot_sync(0xffffffffu, rel <= kRound && rel > lo);
-          cur = rb + (31 - __clz((int)(last | 1u)));
-          break;
-        }
-        rb += 31;
-        lo = hi;
-      }
-      uint32_t wv[kExpandItems];
-#if BFB_EXPAND_DEFER
-#pragma unroll
-      for (int it = 0; it < kExpandItems; ++it)
-        if ((done >> it) & 1u) u[it] = ld_stream_u32(adj + addr[it]);
-#endif
-#pragma unroll
-      for (int it = 0; it < kExpandItems; ++it)
-        wv[it] = ((done >> it) & 1u) ? visited[u[it] >> 5] : 0xFFFFFFFFu;
-#pragma unroll
-      for (int it = 0; it < kExpandItems; ++it) {
-        const uint32_t bit = 1u << (u[it] & 31);
-        if (!(wv[it] & bit)) {
-          atomicOr(&visited[u[it] >> 5], bit);
-          if (kParents) {
-            const uint32_t ro = (rows[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
-            v.parent[u[it]] = __ldg(v.q_v + vs + ro);
-          }
-        }
-      }
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ntiles >= nwarps) {
+    for (int64_t t = gw; t < ntiles; t += nwarps) {
+      const int64_t e0 = t * kTile;
+      const int span = (int)min(kTile, T - e0);
+      const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
+      uint32_t cur = v.tile_vstart[t];
+      for (int k = 0; k * kSub < span; ++k)
+        cur = expand_subtile<kParents>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
+                                       cur, ve, le_mask);
+    }
+  } else {
+    const int64_t nsub = (T + kSub - 1) / kSub;
+    for (int64_t st = gw; st < nsub; st += nwarps) {
+      const int64_t t = st / kSubPerTile;
+      const int64_t r0 = st * kSub;
+      const uint32_t vs = v.tile_vstart[t];
+      const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
+      const uint32_t cur = (st % kSubPerTile) ? find_row(v.q_pre, vs, ve, r0) : vs;
+      expand_subtile<kParents>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask);
     }
   }
 }
 
-#ifndef BFB_EXPAND_WARP
-#define BFB_EXPAND_WARP 1
-#endif
 // Launch phase 1 (top-down) for one part on stream s.
 template <bool kParents>
 void launch_expand(int grid, const PartView& v, const uint32_t* adj, cudaStream_t s) {
-  if (BFB_EXPAND_WARP)
-    k_expand_w<kParents><<<grid, kExpandBlock, 0, s>>>(v, adj);
-  else
-    k_expand<kParents><<<grid, kExpandBlock, expand_smem_bytes<kParents>(), s>>>(v, adj);
+  k_expand_w<kParents><<<grid, kExpandBlock, 0, s>>>(v, adj);
 }
 
 template <bool kParents>
 int expand_occupancy(int* occ) {
-  BFB_CUDA(cudaFuncSetAttribute(k_expand<kParents>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)expand_smem_bytes<kParents>()));
-  if (BFB_EXPAND_WARP)
-    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents>,
-                                                           kExpandBlock, 0));
-  else
-    BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand<kParents>, kExpandBlock,
-                                                           expand_smem_bytes<kParents>()));
+  BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents>, kExpandBlock, 0));
   return BFB_OK;
 }
 
@@ -692,6 +518,25 @@ __global__ void __launch_bounds__(256) k_unit_scan_apply(PartView v) {
   }
 }
 
+// Tile starts of 32 consecutive queue rows (one per lane): tiles whose first
+// edge lies in a row's [e, e + d) start in that row.  Rows spanning many
+// tiles (hubs: up to max_degree / 256) are written by the whole warp.
+__device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vstart, bool ok,
+                                                  int64_t e, int64_t d, int64_t p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = ok ? (e + kTile - 1) / kTile : 0;
+  const int64_t t1 = ok ? (e + d + kTile - 1) / kTile : 0;
+  const bool wide = t1 - t0 > 32;
+  if (!wide)
+    for (int64_t t = t0; t < t1; ++t) tile_vstart[t] = (uint32_t)p;
+  for (unsigned big = __ballot_sync(0xffffffffu, wide); big; big &= big - 1) {
+    const int j = __ffs(big) - 1;
+    const int64_t a = __shfl_sync(0xffffffffu, t0, j), b = __shfl_sync(0xffffffffu, t1, j);
+    const uint32_t pj = (uint32_t)__shfl_sync(0xffffffffu, p, j);
+    for (int64_t t = a + lane; t < b; t += 32) tile_vstart[t] = pj;
+  }
+}
+
 // Write pass, per 32-word unit (1024 vertices) and warp:
 //   1. levels of every new vertex (lane = bit, one coalesced store per word);
 //   2. the owned new vertices compacted into a per-warp shared list in
@@ -753,14 +598,14 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
         }
         inc = x;
       }
+      const int64_t e = ecarry + inc - d;
+      const int64_t p = p0 + k;
       if (ok) {
-        const int64_t e = ecarry + inc - d;
-        const int64_t p = p0 + k;
         v.q_v[p] = u;
         v.q_pre[p] = e;
         v.q_base[p] = o0 - e;
-        for (int64_t t = (e + kTile - 1) / kTile; t * kTile < e + d; ++t) v.tile_vstart[t] = (uint32_t)p;
       }
+      write_tile_starts(v.tile_vstart, ok, e, d, p);
       ecarry += __shfl_sync(0xffffffffu, inc, 31);
     }
     __syncwarp();
@@ -1269,14 +1114,10 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_TRY(expand_occupancy<true>(&occ));
   else
     BFB_TRY(expand_occupancy<false>(&occ));
-  // Developer knobs for tuning runs: cap resident expand blocks per SM and
-  // the shared-memory carveout (percent); unset = occupancy maximum.
+  // Developer knob for tuning runs: cap resident expand blocks per SM
+  // (unset = occupancy maximum).
   if (const char* e = std::getenv("BFB_EXPAND_OCC")) occ = std::min(occ, std::max(1, std::atoi(e)));
-  if (const char* e = std::getenv("BFB_CARVEOUT")) {
-    const int pct = std::atoi(e);
-    BFB_CUDA(cudaFuncSetAttribute(k_expand<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    BFB_CUDA(cudaFuncSetAttribute(k_expand<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-  }
+
   ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
   BFB_TRY(set_l2_window(ctx, ctx->parts[0].visited.p, nwords * sizeof(uint32_t)));
   for (auto& ev : D->ev) BFB_CUDA(cudaEventCreate(&ev));
