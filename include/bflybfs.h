@@ -34,6 +34,8 @@ extern "C" {
 #define BFB_ERR_RANGE (-8)          /* ValueError: endpoint >= num_vertices (graphs.py:44-45) */
 #define BFB_ERR_STATE (-9)          /* RuntimeError: call order (no graph / no engine) */
 #define BFB_ERR_CAPACITY (-10)      /* RuntimeError: buffer-bound violation */
+#define BFB_ERR_PARSE (-11)         /* ValueError (ParseError): malformed text graph, see bfb_parse_result */
+#define BFB_ERR_IO (-12)            /* OSError: file open/read/write failure           */
 #define BFB_ERR_CUDA (-20)          /* RuntimeError: CUDA failure                      */
 #define BFB_ERR_OOM (-21)           /* MemoryError: device allocation failed           */
 
@@ -61,6 +63,19 @@ typedef struct bfb_run_stats {
   int64_t edges_examined;            /* bottom-up levels: edges actually checked      */
   int64_t bottom_up_levels;          /* levels whose phase 1 ran bottom-up            */
 } bfb_run_stats;
+
+/* Outcome of bfb_parse_text (graphs.py:96-202 ParseError carries the line). */
+typedef struct bfb_parse_result {
+  int64_t num_lines;     /* text lines parsed by the device                      */
+  int64_t num_edges;     /* edge lines (entries) kept                            */
+  int64_t max_id_plus1;  /* "edges": 1 + largest vertex id (0 if no edges)      */
+  int64_t err_line;      /* 1-based line of the first error, 0 if none          */
+  int32_t err_code;      /* 2 tokens, 3 non-integer id, 4 negative id, 5/6 src/dst
+                            id > MAX_VID, 7 mtx entry tokens, 8 mtx non-integer,
+                            9 mtx coordinate outside rows x cols                 */
+  int32_t pad;
+  int64_t err_begin, err_end;  /* byte range of the offending line in `data`    */
+} bfb_parse_result;
 
 /* ---- library ---------------------------------------------------------- */
 const char* bfb_version(void);
@@ -101,6 +116,30 @@ int bfb_set_direction(bfb_ctx* ctx, int mode, double alpha, double beta);
  * event, stop records another, synchronizes and returns the elapsed ms. */
 int bfb_timer_start(bfb_ctx* ctx);
 int bfb_timer_stop(bfb_ctx* ctx, double* elapsed_ms_out);
+
+/* ---- text ingestion and the CSR cache (graphs.py:96-209) ----------------- */
+/* load_edge_list's line parsing on device: `data` (host, len bytes) is copied
+ * to HBM and split into lines (newline 0: universal newlines \n, \r\n, \r as
+ * for a path source; 1: \n only, as an io.StringIO source iterates), each
+ * line tokenised and its ids parsed with Python int() rules.  fmt 0 "edges": 'src dst' lines, '#'/'%'
+ * comments.  fmt 1 "mtx": the coordinate entries of a Matrix Market file
+ * (the caller has read the header and size line; `data` starts after them,
+ * line numbers continue from first_line_no, rows/cols bound the entries).
+ * The parsed edges stay in ctx for bfb_graph_from_parsed / bfb_parsed_edges.
+ * A malformed line returns BFB_ERR_PARSE with result->err_* set. */
+int bfb_parse_text(bfb_ctx* ctx, const char* data, int64_t len, int fmt, int newline,
+                   int64_t first_line_no, int64_t rows, int64_t cols, bfb_parse_result* result);
+/* Copy the parsed edges out: 2 * num_edges uint32 (src, dst pairs). */
+int bfb_parsed_edges(bfb_ctx* ctx, uint32_t* edges_out);
+/* CSR from the parsed edges without leaving the device: symmetrize = 1 is
+ * build_csr(symmetrize(el)) (graphs.py:218-251), 0 is build_csr(el). */
+int bfb_graph_from_parsed(bfb_ctx* ctx, int64_t num_vertices, int symmetrize);
+/* write_edge_list (graphs.py:205-209): 'u v\n' lines, byte-identical. */
+int bfb_write_edge_list(const char* path, const uint32_t* edges, int64_t num_edges);
+/* Binary CSR cache of the resident graph ("BFBCSR01", n, m, offsets, adjacency):
+ * save after a build, load instead of re-generating / re-parsing. */
+int bfb_graph_save(bfb_ctx* ctx, const char* path);
+int bfb_graph_load(bfb_ctx* ctx, const char* path);
 
 /* ---- graph-core on device (graphs.py) ------------------------------------ */
 /* generate_rmat (graphs.py:254-285): raw edges to a HOST buffer of 2*m uint32

@@ -22,6 +22,7 @@ BFB_OK = 0
 ERR_INVALID, ERR_ROOT, ERR_PARTITION, ERR_FANOUT = -1, -2, -3, -4
 ERR_SELF_EDGE, ERR_DUPLICATE, ERR_NO_REVERSE, ERR_RANGE = -5, -6, -7, -8
 ERR_STATE, ERR_CAPACITY, ERR_CUDA, ERR_OOM = -9, -10, -20, -21
+ERR_PARSE, ERR_IO = -11, -12
 
 STRATEGY = {"butterfly": 0, "all2all": 1, "all-to-all": 1, "all_to_all": 1}
 DIRECTION = {"top-down": 0, "topdown": 0, "optimizing": 1, "direction-optimizing": 1,
@@ -46,6 +47,19 @@ class RunStatsC(ctypes.Structure):
         ("kernel_launches", c_int64),
         ("edges_examined", c_int64),
         ("bottom_up_levels", c_int64),
+    ]
+
+
+class ParseResultC(ctypes.Structure):
+    _fields_ = [
+        ("num_lines", c_int64),
+        ("num_edges", c_int64),
+        ("max_id_plus1", c_int64),
+        ("err_line", c_int64),
+        ("err_code", c_int32),
+        ("pad", c_int32),
+        ("err_begin", c_int64),
+        ("err_end", c_int64),
     ]
 
 
@@ -89,6 +103,13 @@ _SIGNATURES = {
     "bfb_copy_parents": (c_int, [c_void_p, _I64P]),
     "bfb_validate": (c_int, [c_void_p, c_int64, _I64P]),
     "bfb_probe_peak": (c_int, [c_void_p, c_int64, _I64P, POINTER(c_double)]),
+    "bfb_parse_text": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int64, c_int64,
+                               c_int64, POINTER(ParseResultC)]),
+    "bfb_parsed_edges": (c_int, [c_void_p, _U32P]),
+    "bfb_graph_from_parsed": (c_int, [c_void_p, c_int64, c_int]),
+    "bfb_write_edge_list": (c_int, [c_char_p, _U32P, c_int64]),
+    "bfb_graph_save": (c_int, [c_void_p, c_char_p]),
+    "bfb_graph_load": (c_int, [c_void_p, c_char_p]),
     "bfb_rank_setup": (c_int, [c_void_p, c_int, _I64P, c_int, c_int, c_int, c_int]),
     "bfb_rank_ipc_handles": (c_int, [c_void_p, c_void_p]),
     "bfb_rank_open_peer": (c_int, [c_void_p, c_int, c_void_p]),
@@ -138,6 +159,10 @@ def check(rc):
     if rc in (ERR_INVALID, ERR_ROOT, ERR_PARTITION, ERR_FANOUT, ERR_SELF_EDGE, ERR_DUPLICATE,
               ERR_NO_REVERSE, ERR_RANGE):
         raise ValueError(msg)
+    if rc == ERR_PARSE:
+        raise ValueError(msg)
+    if rc == ERR_IO:
+        raise OSError(msg)
     if rc == ERR_OOM:
         raise MemoryError(msg)
     raise RuntimeError(msg)

@@ -35,32 +35,11 @@ def _load_graph(args):
         return g, f"kronecker-s{s}-ef{ef}-seed{seed}"
     if not args.graph:
         raise SystemExit("need --graph PATH or --kronecker SCALE EF SEED")
-    el = load_edge_list(args.graph, args.format)
-    g = graphs.build_csr(graphs.symmetrize(el))
-    return g, args.graph
-
-
-def load_edge_list(path, fmt="edges"):
-    """Minimal reader for the two SPEC formats; the
-    reference's full parser (graphs.py:96-202) is out of this path's scope."""
-    rows, n_decl = [], None
-    with open(path, "rt", encoding="ascii", errors="replace") as fh:
-        if fmt == "mtx":
-            header = fh.readline().strip().lower().split()
-            if len(header) < 4 or header[0] != "%%matrixmarket":
-                raise ValueError("expected '%%MatrixMarket matrix coordinate' header")
-        for line in fh:
-            t = line.strip()
-            if not t or t[0] in "#%":
-                continue
-            parts = t.split()
-            if fmt == "mtx" and n_decl is None:
-                n_decl = max(int(parts[0]), int(parts[1]))
-                continue
-            rows.append((int(parts[0]) - (fmt == "mtx"), int(parts[1]) - (fmt == "mtx")))
-    e = np.asarray(rows, dtype=np.int64).reshape(-1, 2)
-    n = n_decl if n_decl is not None else (int(e.max()) + 1 if e.size else 0)
-    return graphs.EdgeList(e.astype(np.uint32), n)
+    # parse -> symmetrize -> CSR on device (graphs.load_graph); a .bfbcsr
+    # cache written by `generate --out NAME.bfbcsr` loads directly
+    if args.graph.endswith(".bfbcsr"):
+        return graphs.load_csr(args.graph), args.graph
+    return graphs.load_graph(args.graph, args.format), args.graph
 
 
 def sample_roots(n, count, seed):
@@ -150,8 +129,10 @@ def cmd_schedule(args):
 def cmd_generate(args):
     s, ef, seed = args.kronecker
     g = graphs.kronecker(int(s), int(ef), int(seed))
-    e = g.device.edges()
-    np.savetxt(args.out, e, fmt="%d")
+    if args.out.endswith(".bfbcsr"):
+        graphs.save_csr(g, args.out)  # binary CSR cache
+    else:
+        graphs.write_edge_list(graphs.EdgeList(g.device.edges(), g.num_vertices), args.out)
     print(json.dumps({"num_vertices": g.num_vertices, "num_edges": g.num_edges, "out": args.out}))
     return 0
 

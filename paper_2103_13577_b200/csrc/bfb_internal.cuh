@@ -216,6 +216,9 @@ struct bfb_ctx {
   std::vector<int64_t> last_sizes;     // per_level_frontier_size of the last run
   int64_t launches = 0;
   cudaEvent_t timer[2] = {nullptr, nullptr};
+  // text ingestion: edges parsed by bfb_parse_text, awaiting the CSR build
+  bfb::DevBuf<uint2> parsed;
+  int64_t parsed_m = 0;
 };
 
 namespace bfb {
@@ -228,6 +231,15 @@ int build_from_edges(bfb_ctx* ctx, int64_t n, const uint32_t* host_edges, int64_
 int rmat_to_host(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc, const uint64_t thr[3],
                  uint32_t* out);
 int load_csr(bfb_ctx* ctx, int64_t n, int64_t m, const int64_t* offsets, const uint32_t* adj);
+int build_from_device_edges(bfb_ctx* ctx, int64_t n, DevBuf<uint2>& edges, int64_t m,
+                            bool symmetrize);
+// ingest.cu
+int parse_text(bfb_ctx* ctx, const char* data, int64_t len, int fmt, int nl, int64_t line0,
+               int64_t rows, int64_t cols, bfb_parse_result* res);
+int parsed_copy(bfb_ctx* ctx, uint32_t* out);
+int write_edge_list(const char* path, const uint32_t* edges, int64_t m);
+int graph_save(bfb_ctx* ctx, const char* path);
+int graph_load(bfb_ctx* ctx, const char* path);
 int copy_edges(bfb_ctx* ctx, uint32_t* out);
 int partition_1d(bfb_ctx* ctx, int parts, int64_t* out);
 int count_nonisolated(bfb_ctx* ctx, int64_t* out);

@@ -344,6 +344,47 @@ int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out) {
   return engine_validate(ctx, root, errors_out);
 }
 
+int bfb_parse_text(bfb_ctx* ctx, const char* data, int64_t len, int fmt, int newline,
+                   int64_t first_line_no, int64_t rows, int64_t cols, bfb_parse_result* result) {
+  CTX_GUARD(ctx);
+  if (!result || len < 0 || (len && !data) || (fmt != 0 && fmt != 1) || first_line_no < 0 ||
+      (newline != 0 && newline != 1))
+    return fail(BFB_ERR_INVALID, "bad arguments");
+  return parse_text(ctx, data, len, fmt, newline, first_line_no, rows, cols, result);
+}
+
+int bfb_parsed_edges(bfb_ctx* ctx, uint32_t* edges_out) {
+  CTX_GUARD(ctx);
+  if (!edges_out && ctx->parsed_m) return fail(BFB_ERR_INVALID, "null output");
+  return parsed_copy(ctx, edges_out);
+}
+
+int bfb_graph_from_parsed(bfb_ctx* ctx, int64_t num_vertices, int symmetrize) {
+  CTX_GUARD(ctx);
+  if (!ctx->parsed.p) return fail(BFB_ERR_STATE, "no parsed edges");
+  bfb::DevBuf<uint2> edges(std::move(ctx->parsed));
+  const int64_t m = ctx->parsed_m;
+  ctx->parsed_m = 0;
+  return build_from_device_edges(ctx, num_vertices, edges, m, symmetrize != 0);
+}
+
+int bfb_write_edge_list(const char* path, const uint32_t* edges, int64_t num_edges) {
+  if (!path || num_edges < 0 || (num_edges && !edges)) return fail(BFB_ERR_INVALID, "bad arguments");
+  return write_edge_list(path, edges, num_edges);
+}
+
+int bfb_graph_save(bfb_ctx* ctx, const char* path) {
+  CTX_GUARD(ctx);
+  if (!path) return fail(BFB_ERR_INVALID, "null path");
+  return graph_save(ctx, path);
+}
+
+int bfb_graph_load(bfb_ctx* ctx, const char* path) {
+  CTX_GUARD(ctx);
+  if (!path) return fail(BFB_ERR_INVALID, "null path");
+  return graph_load(ctx, path);
+}
+
 int bfb_probe_peak(bfb_ctx* ctx, int64_t bytes, int64_t* probes_out, double* ms_out) {
   CTX_GUARD(ctx);
   if (!probes_out || !ms_out || bytes <= 0) return fail(BFB_ERR_INVALID, "bad arguments");

@@ -527,10 +527,22 @@ int build_from_edges(bfb_ctx* ctx, int64_t n, const uint32_t* host_edges, int64_
   if (n > (int64_t(1) << 32)) return fail(BFB_ERR_INVALID, "num_vertices exceeds the VID range");
   engine_release(ctx);
   ctx->g = DevGraph();
-  cudaStream_t s = ctx->stream;
   DevBuf<uint2> edges;
   BFB_TRY(edges.alloc(m));
-  if (m) BFB_CUDA(cudaMemcpyAsync(edges.p, host_edges, m * sizeof(uint2), cudaMemcpyHostToDevice, s));
+  if (m)
+    BFB_CUDA(cudaMemcpyAsync(edges.p, host_edges, m * sizeof(uint2), cudaMemcpyHostToDevice,
+                             ctx->stream));
+  return build_from_device_edges(ctx, n, edges, m, symmetrize);
+}
+
+// symmetrize (optional) + build_csr from an edge array already in HBM.
+int build_from_device_edges(bfb_ctx* ctx, int64_t n, DevBuf<uint2>& edges, int64_t m,
+                            bool symmetrize) {
+  if (n < 0 || m < 0) return fail(BFB_ERR_INVALID, "negative size");
+  if (n > (int64_t(1) << 32)) return fail(BFB_ERR_INVALID, "num_vertices exceeds the VID range");
+  engine_release(ctx);
+  ctx->g = DevGraph();
+  cudaStream_t s = ctx->stream;
   DevBuf<uint32_t> deg;
   BFB_TRY(deg.alloc(n));
   BFB_CUDA(cudaMemsetAsync(deg.p, 0, n * sizeof(uint32_t), s));

@@ -2,8 +2,10 @@
 
 Same names, argument meaning and exceptions as the reference module; the
 generator, symmetrize, CSR build and partition run as sm_100a kernels
-(include/bflybfs.h).  Text ingestion (graphs.py:96-209) is outside the hot
-path and is not provided.
+(include/bflybfs.h).  Text ingestion (graphs.py:96-209) tokenises
+and parses the file on device (csrc/ingest.cu); ``load_graph`` goes from text
+to a device-resident CSR without the edges visiting the host, and
+``save_csr`` / ``load_csr`` keep a binary CSR cache.
 """
 
 from __future__ import annotations
@@ -18,6 +20,14 @@ VID = np.uint32                      # graphs.py:13
 MAX_VID = int(np.iinfo(VID).max)     # graphs.py:14
 UNREACHED = MAX_VID                  # graphs.py:17
 RMAT_PROBS = (0.57, 0.19, 0.19, 0.05)  # graphs.py:21
+
+
+class ParseError(ValueError):
+    """Malformed graph input; carries the 1-based line number (graphs.py:24-29)."""
+
+    def __init__(self, message, line_no):
+        super().__init__(f"line {line_no}: {message}")
+        self.line_no = line_no
 
 
 class EdgeList:
@@ -216,3 +226,191 @@ def sample_roots(g, count=64, seed=2103):
     k = min(int(count), pop)
     ranks = np.random.default_rng(seed).choice(pop, k, replace=False)
     return dg.select_nonisolated(ranks)
+
+
+# ------------------------------------------------------------ text ingestion --
+_FMT = {"edges": 0, "mtx": 1}
+
+
+def _source_bytes(source):
+    """(bytes, decode, newline mode) for a path, a text stream or a binary
+    stream, read the way the reference reads it (graphs.py:96-101): paths and
+    binary streams as ASCII with errors replaced and universal newlines; a
+    text stream line by line as it iterates itself (io.StringIO splits on
+    "\n" only)."""
+    import io
+    from pathlib import Path
+
+    ascii_ = lambda b: b.decode("ascii", errors="replace")  # noqa: E731
+    if isinstance(source, (str, Path)):
+        with open(source, "rb") as fh:
+            return fh.read(), ascii_, 0
+    if isinstance(source, io.TextIOBase):
+        text = "".join(source)
+        return text.encode("utf-8"), lambda b: b.decode("utf-8", errors="replace"), 1
+    return source.read(), ascii_, 0
+
+
+def _next_line(data, pos, nl=0):
+    """The line starting at pos: (line bytes, next pos); nl = 0 universal
+    newlines, 1 "\n" only."""
+    n = len(data)
+    i = pos
+    stops = (10, 13) if nl == 0 else (10,)
+    while i < n and data[i] not in stops:
+        i += 1
+    if i >= n:
+        return data[pos:n], n
+    return data[pos:i], i + (2 if data[i] == 13 and i + 1 < n and data[i + 1] == 10 else 1)
+
+
+def _mtx_prologue(data, decode, nl=0):
+    """Header and size line of a Matrix Market file, as graphs.py:138-164.
+    Returns (entry offset, line number of the size line, rows, cols, nnz)."""
+    header, pos = _next_line(data, 0, nl) if data else (b"", 0)
+    tokens = decode(header).strip().lower().split()
+    if len(tokens) < 4 or tokens[0] != "%%matrixmarket" or tokens[1] != "matrix" \
+            or tokens[2] != "coordinate":
+        raise ParseError("expected '%%MatrixMarket matrix coordinate' header", 1)
+    line_no = 1
+    while pos < len(data):
+        line, pos = _next_line(data, pos, nl)
+        line_no += 1
+        stripped = decode(line).strip()
+        if not stripped or stripped[0] == "%":
+            continue
+        parts = stripped.split()
+        if len(parts) != 3:
+            raise ParseError("expected 'rows cols nnz' size line", line_no)
+        try:
+            rows, cols, nnz = (int(p) for p in parts)
+        except ValueError:
+            raise ParseError("non-integer size line", line_no) from None
+        return pos, line_no, rows, cols, nnz
+    raise ParseError("missing size line", line_no + 1)
+
+
+def _raise_line_error(res, data, decode, rows=0, cols=0):
+    """The reference's ParseError for the first malformed line the device
+    found (graphs.py:109-134, 165-180)."""
+    stripped = decode(bytes(data[res.err_begin:res.err_end])).strip()
+    parts = stripped.split()
+    code, ln = res.err_code, res.err_line
+    if code == 2:
+        raise ParseError(f"expected 'src dst', got {stripped!r}", ln)
+    if code == 3:
+        raise ParseError(f"non-integer vertex id in {stripped!r}", ln)
+    if code == 4:
+        raise ParseError(f"negative vertex id in {stripped!r}", ln)
+    if code in (5, 6):
+        raise ParseError(f"vertex id {int(parts[code - 5])} exceeds the representable range", ln)
+    if code == 7:
+        raise ParseError(f"expected coordinate entry, got {stripped!r}", ln)
+    if code == 8:
+        raise ParseError(f"non-integer coordinate in {stripped!r}", ln)
+    if code == 9:
+        i, j = int(parts[0]), int(parts[1])
+        raise ParseError(f"coordinate ({i}, {j}) outside {rows}x{cols}", ln)
+    raise RuntimeError(f"unknown parse error code {code} at line {ln}")
+
+
+def _parse_on_device(dg, source, fmt):
+    """Parse ``source`` into dg's parsed-edge buffer; returns (num_edges,
+    num_vertices) with the reference's validation and errors."""
+    import ctypes
+
+    from . import _lib
+
+    if fmt not in _FMT:
+        raise ValueError(f"unknown format {fmt!r}")
+    data, decode, nl = _source_bytes(source)
+    start, line0, rows, cols, nnz = 0, 0, 0, 0, None
+    if fmt == "mtx":
+        start, line0, rows, cols, nnz = _mtx_prologue(data, decode, nl)
+    region = np.frombuffer(data, dtype=np.uint8)[start:]
+    clamp = 1 << 40  # any entry above 2^32 is outside the VID range anyway
+    res = _lib.ParseResultC()
+    rc = _lib.load().bfb_parse_text(dg.handle, region.ctypes.data if region.size else None,
+                                    int(region.size), _FMT[fmt], nl, int(line0),
+                                    max(-1, min(int(rows), clamp)), max(-1, min(int(cols), clamp)),
+                                    ctypes.byref(res))
+    if rc == _lib.ERR_PARSE:
+        _raise_line_error(res, region, decode, rows, cols)
+    _lib.check(rc)
+    m = int(res.num_edges)
+    if fmt == "edges":
+        return m, int(res.max_id_plus1)
+    if m != nnz:
+        raise ParseError(f"declared {nnz} entries, found {m}", line0 + int(res.num_lines) + 1)
+    top = max(rows, cols)
+    if top and top - 1 > MAX_VID:
+        raise ParseError(f"vertex id {top - 1} exceeds the representable range", 1)
+    return m, (top if top else 0)
+
+
+def load_edge_list(source, fmt="edges", device=0):
+    """graphs.py:185-202: directed edges from a path or stream ("edges": 'src
+    dst' lines, '#'/'%' comments, 0-based; "mtx": Matrix Market coordinate
+    pattern, 1-based ids shifted).  Tokenising and integer parsing run on
+    device; same EdgeList, num_vertices and ParseError (line numbers and
+    messages) as the reference."""
+    import ctypes
+
+    from . import _lib
+
+    dg = DeviceGraph(device)
+    try:
+        m, n = _parse_on_device(dg, source, fmt)
+        out = np.empty((m, 2), dtype=VID)
+        _lib.check(_lib.load().bfb_parsed_edges(dg.handle, _lib.ptr(out, ctypes.c_uint32)))
+    finally:
+        dg.close()
+    return EdgeList(out, n)
+
+
+def load_graph(source, fmt="edges", device=0):
+    """build_csr(symmetrize(load_edge_list(source, fmt))) with the edges never
+    leaving the device: parse, mirror/dedup and CSR all in HBM."""
+    from . import _lib
+
+    dg = DeviceGraph(device)
+    try:
+        m, n = _parse_on_device(dg, source, fmt)
+        _lib.check(_lib.load().bfb_graph_from_parsed(dg.handle, int(n), 1))
+        dg._refresh()
+    except BaseException:
+        dg.close()
+        raise
+    return Graph.from_device(dg)
+
+
+def write_edge_list(el, path):
+    """graphs.py:205-209: 'src dst' text lines, byte-identical output."""
+    import ctypes
+
+    from . import _lib
+
+    e = np.ascontiguousarray(el.edges, dtype=VID)
+    _lib.check(_lib.load().bfb_write_edge_list(str(path).encode(), _lib.ptr(e, ctypes.c_uint32),
+                                               int(e.shape[0])))
+
+
+def save_csr(g, path):
+    """Binary CSR cache of ``g`` ("BFBCSR01" header, n, m, offsets, adjacency)."""
+    from . import _lib
+
+    _lib.check(_lib.load().bfb_graph_save(device_graph(g).handle, str(path).encode()))
+
+
+def load_csr(path, device=0):
+    """A Graph from a save_csr cache, resident on ``device``."""
+    from . import _lib
+
+    dg = DeviceGraph(device)
+    try:
+        _lib.check(_lib.load().bfb_graph_load(dg.handle, str(path).encode()))
+        dg._refresh()
+    except BaseException:
+        dg.close()
+        raise
+    return Graph.from_device(dg)

@@ -128,3 +128,24 @@ def test_pcg_draw_layout():
     # integer thresholds == float compare for every representable 53-bit draw edge
     for p, t in zip((pb, prt, prb), ints):
         assert (t - 1) * 2.0 ** -53 < p <= t * 2.0 ** -53
+
+
+def test_parse_golden_matches_live_reference(reference_graphs, tmp_path):
+    # the committed parse fixtures still equal the reference's own parser
+    import base64
+    import json
+    import os
+
+    from tests.util import sha16
+
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                        "parse_golden.json")))["cases"]
+    for c in cases:
+        p = tmp_path / c["name"]
+        p.write_bytes(base64.b64decode(c["data_b64"]))
+        try:
+            el = reference_graphs.load_edge_list(str(p), c["fmt"])
+            assert "error" not in c, c["name"]
+            assert sha16(el.edges) == c["edges_sha"] and el.num_vertices == c["num_vertices"]
+        except reference_graphs.ParseError as e:
+            assert str(e) == c["error"], c["name"]
