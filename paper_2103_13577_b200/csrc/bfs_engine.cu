@@ -22,6 +22,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 
 #include "bfb_device.cuh"
 #include "bfb_internal.cuh"
@@ -403,13 +405,26 @@ __device__ __forceinline__ void unit_word(const PartView& v, int64_t unit, int l
   own = nb & owned_mask(w, v.lo, v.hi);
 }
 
+// Degree sum of the vertices whose bits are set in x (vertex ids vbase + bit),
+// four bits per step so eight offsets loads are in flight at once.
 __device__ __forceinline__ int64_t word_degree_sum(uint32_t x, int64_t vbase,
                                                    const int64_t* __restrict__ off) {
   int64_t d = 0;
   while (x) {
-    const int b = __ffs(x) - 1;
-    x &= x - 1;
-    d += __ldg(off + vbase + b + 1) - __ldg(off + vbase + b);
+    int b[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      b[k] = x ? __ffs(x) - 1 : -1;
+      x &= x - 1;
+    }
+    int64_t lo[4], hi[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      lo[k] = b[k] >= 0 ? __ldg(off + vbase + b[k]) : 0;
+      hi[k] = b[k] >= 0 ? __ldg(off + vbase + b[k] + 1) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d += hi[k] - lo[k];
   }
   return d;
 }
@@ -549,9 +564,9 @@ __device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vs
 template <bool kWide>
 __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
                                                       uint32_t next_level) {
-  __shared__ uint32_t s_list[256 / 32][1024];
+  __shared__ uint16_t s_list[256 / 32][1024];  // unit-local vertex index (word * 32 + bit)
   const int lane = threadIdx.x & 31;
-  uint32_t* list = s_list[threadIdx.x >> 5];
+  uint16_t* list = s_list[threadIdx.x >> 5];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -576,14 +591,14 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
     }
     const int total = __shfl_sync(0xffffffffu, pos, 31);
     pos -= cnt;
-    for (uint32_t x = own; x; x &= x - 1) list[pos++] = (uint32_t)(((w0 + lane) << 5) + __ffs(x) - 1);
+    for (uint32_t x = own; x; x &= x - 1) list[pos++] = (uint16_t)((lane << 5) + __ffs(x) - 1);
     __syncwarp();
     const int64_t p0 = v.upos[unit];
     int64_t ecarry = v.uepre[unit];
     for (int i = 0; i < total; i += 32) {
       const int k = i + lane;
       const bool ok = k < total;
-      const uint32_t u = ok ? list[k] : 0u;
+      const uint32_t u = ok ? (uint32_t)((w0 << 5) + list[k]) : 0u;
       const int64_t o0 = ok ? __ldg(off + u) : 0;
       const int64_t d = ok ? __ldg(off + u + 1) - o0 : 0;
       int64_t inc;
@@ -842,6 +857,31 @@ __global__ void k_validate(const int64_t* __restrict__ off, const uint32_t* __re
   }
 }
 
+// Grid of a grid-stride kernel: one full wave of resident CTAs (148 SMs x the
+// kernel's occupancy), fewer if the work is smaller.  Occupancy is queried
+// once per kernel.
+template <class K>
+unsigned resident_grid(K kernel, int64_t work, int block, int num_sms, size_t smem = 0) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> occ_of;
+  int occ = 1;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ_of.find((const void*)kernel);
+    if (it == occ_of.end()) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem) != cudaSuccess)
+        occ = 4;
+      occ = std::max(1, occ);
+      occ_of[(const void*)kernel] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  int64_t g = (work + block - 1) / block;
+  g = std::min<int64_t>(g, (int64_t)num_sms * occ);
+  return (unsigned)std::max<int64_t>(1, g);
+}
+
 unsigned grid_cap(int64_t work, int block, int num_sms, int per_sm = 8) {
   int64_t g = (work + block - 1) / block;
   int64_t cap = (int64_t)num_sms * per_sm;
@@ -877,7 +917,7 @@ __global__ void k_merge_peers(SrcList L, uint32_t* __restrict__ vis, int64_t nwo
 int launch_commit_count(const PartView& v, const int64_t* off, RunCounters* run, int sms,
                         cudaStream_t s) {
   const int64_t ntiles = std::max<int64_t>(1, (v.nunits + kScanTile - 1) / kScanTile);
-  k_commit_count<<<grid_cap(v.nunits * 32, 256, sms, 8), 256, 0, s>>>(v, off);
+  k_commit_count<<<resident_grid(k_commit_count, v.nunits * 32, 256, sms), 256, 0, s>>>(v, off);
   k_unit_scan_reduce<<<(unsigned)ntiles, 256, 0, s>>>(v);
   k_unit_scan_tiles<<<1, 1024, 0, s>>>(v, ntiles, run);
   return 3;
@@ -889,16 +929,18 @@ int launch_commit_count(const PartView& v, const int64_t* off, RunCounters* run,
 int launch_commit_write(const PartView& v, const int64_t* off, uint32_t next_level, bool with_queue,
                         int sms, cudaStream_t s) {
   const int64_t ntiles = std::max<int64_t>(1, (v.nunits + kScanTile - 1) / kScanTile);
-  const unsigned grid = grid_cap(v.nunits * 32, 256, sms, 8);
+  const int64_t work = v.nunits * 32;
   if (!with_queue) {
-    k_commit_light<<<grid, 256, 0, s>>>(v, next_level);
+    k_commit_light<<<resident_grid(k_commit_light, work, 256, sms), 256, 0, s>>>(v, next_level);
     return 1;
   }
   k_unit_scan_apply<<<(unsigned)ntiles, 256, 0, s>>>(v);
   if (v.wide)
-    k_commit_write<true><<<grid, 256, 0, s>>>(v, off, next_level);
+    k_commit_write<true><<<resident_grid(k_commit_write<true>, work, 256, sms), 256, 0, s>>>(
+        v, off, next_level);
   else
-    k_commit_write<false><<<grid, 256, 0, s>>>(v, off, next_level);
+    k_commit_write<false><<<resident_grid(k_commit_write<false>, work, 256, sms), 256, 0, s>>>(
+        v, off, next_level);
   return 2;
 }
 
@@ -906,7 +948,8 @@ int launch_commit_write(const PartView& v, const int64_t* off, uint32_t next_lev
 // top-down level, from the frontier bitmap, by count -> scan -> write.
 int launch_commit_light_count(const PartView& v, const int64_t* off, uint32_t next_level,
                               RunCounters* run, int sms, cudaStream_t s) {
-  k_commit_light_count<<<grid_cap(v.nunits * 32, 256, sms, 8), 256, 0, s>>>(v, off, next_level, run);
+  k_commit_light_count<<<resident_grid(k_commit_light_count, v.nunits * 32, 256, sms), 256, 0, s>>>(
+      v, off, next_level, run);
   return 1;
 }
 
@@ -1114,9 +1157,15 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_TRY(expand_occupancy<true>(&occ));
   else
     BFB_TRY(expand_occupancy<false>(&occ));
-  // Developer knob for tuning runs: cap resident expand blocks per SM
-  // (unset = occupancy maximum).
+  // Developer knobs for tuning runs: cap resident expand blocks per SM, and
+  // the expand's shared-memory carveout in percent (it uses none; unset =
+  // driver default).
   if (const char* e = std::getenv("BFB_EXPAND_OCC")) occ = std::min(occ, std::max(1, std::atoi(e)));
+  if (const char* e = std::getenv("BFB_CARVEOUT")) {
+    const int pct = std::atoi(e);
+    BFB_CUDA(cudaFuncSetAttribute(k_expand_w<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    BFB_CUDA(cudaFuncSetAttribute(k_expand_w<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  }
 
   ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
   BFB_TRY(set_l2_window(ctx, ctx->parts[0].visited.p, nwords * sizeof(uint32_t)));
