@@ -14,16 +14,17 @@ g = graphs.kronecker(scale, 8, 1)
 dg = g.device
 roots = graphs.sample_roots(g, 6)
 for parents, direction in ((False, "top-down"), (True, "top-down"), (True, "optimizing"), (False, "optimizing")):
-    dg.setup(dg.partition_1d(1), 1, "butterfly", parents=parents)
+    P = int(os.environ.get("SW_PARTS", "1"))
+    dg.setup(dg.partition_1d(P), min(2, P), "butterfly", parents=parents)
     dg.set_direction(direction, float(os.environ.get("SW_ALPHA", "14")), float(os.environ.get("SW_BETA", "24")))
     dg.set_timing(True)
     dg.bfs(int(roots[0]), levels=False)
-    t = []; ex = []; cm = []
+    t = []; ex = []; cm = []; xc = []
     for r in roots:
         _, _, sizes, st, _ = dg.bfs(int(r), levels=False)
-        t.append(st.traversed_edges / st.elapsed_ms / 1e6); ex.append(st.expand_ms); cm.append(st.commit_ms)
+        t.append(st.traversed_edges / st.elapsed_ms / 1e6); ex.append(st.expand_ms); cm.append(st.commit_ms); xc.append(st.exchange_ms)
     hm = len(t) / sum(1 / x for x in t)
-    print(f"{os.environ.get('SW_TAG')}: {direction} parents={parents} hmean={hm:.1f} GTEP/s expand={sum(ex)/len(ex):.2f} ms commit={sum(cm)/len(cm):.2f} ms bu_levels={st.bottom_up_levels} examined={st.edges_examined}", flush=True)
+    print(f"{os.environ.get('SW_TAG')}: {direction} parents={parents} hmean={hm:.1f} GTEP/s expand={sum(ex)/len(ex):.2f} ms commit={sum(cm)/len(cm):.2f} ms exchange={sum(xc)/len(xc):.2f} ms bu_levels={st.bottom_up_levels} examined={st.edges_examined}", flush=True)
 ''' % ROOT
 
 if __name__ == "__main__":
