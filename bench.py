@@ -463,8 +463,9 @@ def run_reference(args, cfg, n_gpus):
                          "kind": "port",
                          "sample": f"each step: oracle/bfs_omp.c top-down BFS (C + OpenMP "
                                    f"restatement of SPEC.md:136-163, {cpu_threads()} threads) from "
-                                   f"the next root, stopped after {budget:.2f} s; input graph built "
-                                   f"on device (generator only) and copied to host "
+                                   f"the next root, stopped after {budget:.2f} s; input graph "
+                                   f"(generator, symmetrize, CSR) built on device outside the "
+                                   f"timed region and copied to host "
                                    f"({build_s:.1f} s incl. {copy_s:.1f} s copy)",
                          "host_threads_available": cpu_threads()},
         "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,

@@ -233,3 +233,48 @@ def test_scale24_golden(golden):
     for r, want in e["bfs"].items():
         lv, _, sizes, st, _ = dg.bfs(int(r))
         assert sha16(lv) == want["levels_sha"] and sizes == want["sizes"]
+
+
+@pytest.mark.slow
+def test_config3_s27_ef16_butterfly_parts():
+    """BASELINE config 3 at full size (Kronecker s27 ef16, fanout 2) with 2
+    and 4 butterfly nodes as parts of one GPU: levels identical to the
+    single-node run, device certificate, rounds = levels x ceil(log2 CN), and
+    the per-round incoming snapshot within the f * |V| bound."""
+    g = graphs.kronecker(27, 16, 1)
+    dg = g.device
+    r = int(graphs.sample_roots(g, 1)[0])
+    dg.setup(dg.partition_1d(1), 1, "butterfly", parents=True)
+    ref, _, sizes, _, _ = dg.bfs(r)
+    assert dg.validate(r) == 0
+    want = sha16(ref)
+    del ref
+    for cn in (2, 4):
+        dg.setup(dg.partition_1d(cn), 2, "butterfly", parents=True)
+        lv, _, s2, st, hw = dg.bfs(r)
+        assert sha16(lv) == want and s2 == sizes
+        assert dg.validate(r) == 0
+        assert st.rounds_executed == len(sizes) * {2: 1, 4: 2}[cn]
+        assert max(hw) <= 2 * g.num_vertices
+
+
+@pytest.mark.slow
+def test_config4_s28_ef8_fanout_sweep():
+    """BASELINE config 4 at full size (Kronecker s28 ef8, 8 nodes) on one GPU
+    (8 parts): fanout 2/4/8 give the same levels and frontier sizes, rounds
+    per level 3/2/1, and fanout 8 (all-to-all) moves CN*(CN-1) transfers per
+    non-trivial level at most."""
+    g = graphs.kronecker(28, 8, 1)
+    dg = g.device
+    r = int(graphs.sample_roots(g, 1)[0])
+    b = dg.partition_1d(8)
+    ref = None
+    for f, rounds in ((2, 3), (4, 2), (8, 1)):
+        dg.setup(b, f, "butterfly")
+        lv, _, sizes, st, _ = dg.bfs(r)
+        key = (sha16(lv), tuple(sizes))
+        ref = ref or key
+        assert key == ref, f
+        assert st.rounds_executed == len(sizes) * rounds
+        assert st.remote_messages <= len(sizes) * 8 * 7
+        assert dg.validate(r) == 0
