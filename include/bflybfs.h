@@ -62,6 +62,9 @@ typedef struct bfb_run_stats {
   int64_t kernel_launches;           /* all kernels this library launched in the run  */
   int64_t edges_examined;            /* bottom-up levels: edges actually checked      */
   int64_t bottom_up_levels;          /* levels whose phase 1 ran bottom-up            */
+  double expand_max_part_ms;         /* timing mode, CN > 1 in one context: sum over
+                                        levels of the slowest node's phase 1 (the
+                                        critical path if each node had its own GPU) */
 } bfb_run_stats;
 
 /* Outcome of bfb_parse_text (graphs.py:96-202 ParseError carries the line). */

@@ -47,6 +47,7 @@ class RunStatsC(ctypes.Structure):
         ("kernel_launches", c_int64),
         ("edges_examined", c_int64),
         ("bottom_up_levels", c_int64),
+        ("expand_max_part_ms", c_double),
     ]
 
 

@@ -706,25 +706,37 @@ __global__ void __launch_bounds__(256) k_commit_light(PartView v, uint32_t next_
   }
 }
 
-__global__ void k_commit_rest(PartView v, uint32_t next_level) {
+// Commit of the words outside this node's owned range (its replicated
+// d_local): levels of the new vertices, start := visited, the
+// frontier bitmap and the frontier count.  Warp = 32 consecutive words
+// (lane = word for the bitmaps, lane = bit for the coalesced level stores).
+__global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_level) {
+  const int lane = threadIdx.x & 31;
+  const int64_t span = v.nwords - (v.whi - v.wlo);  // words outside [wlo, whi)
+  const int64_t nunits = (span + 31) / 32;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t fr = 0;
-  const int64_t span = v.nwords - (v.whi - v.wlo);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < span;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t unit = gw; unit < nunits; unit += nw) {
+    const int64_t i = unit * 32 + lane;
     const int64_t w = i < v.wlo ? i : i + (v.whi - v.wlo);
-    const uint32_t a = v.visited[w];
-    const uint32_t nbits = a & ~v.start[w];
-    if (!nbits) continue;
-    fr += __popc(nbits);
-    const int64_t vb = w << 5;
-    uint32_t x = nbits;
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      v.level[vb + b] = next_level;
+    const bool in = i < span;
+    const uint32_t a = in ? v.visited[w] : 0u;
+    const uint32_t nb = a & ~(in ? v.start[w] : 0u);
+    unsigned m = __ballot_sync(0xffffffffu, nb != 0);
+    if (!m) continue;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
+      const int64_t wj = __shfl_sync(0xffffffffu, w, j);
+      if ((x >> lane) & 1u) v.level[(wj << 5) + lane] = next_level;
     }
-    v.start[w] = a;
-    if (v.front) v.front[w] = nbits;
+    if (nb) {
+      fr += __popc(nb);
+      v.start[w] = a;
+      if (v.front) v.front[w] = nb;
+    }
   }
   __shared__ int64_t red[32];
   fr = block_sum_i64(fr, red);
@@ -977,6 +989,7 @@ struct EngineTables {
   std::vector<RoundDesc> rounds;
   DevBuf<uint32_t> parents_final;  // assembled output parents when num_parts > 1
   cudaEvent_t ev[6] = {};
+  std::vector<cudaEvent_t> part_ev;  // timing mode, CN > 1: per-node phase-1 bounds
   // multi-process mode (rank >= 0): this context holds node `rank` only
   int rank = -1;
   std::vector<const uint32_t*> peer_pub[2];  // per node, by round parity
@@ -997,6 +1010,7 @@ struct EngineTables {
     for (void* p : opened) cudaIpcCloseMemHandle(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : part_ev) cudaEventDestroy(e);
   }
 };
 
@@ -1170,6 +1184,10 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
   ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
   BFB_TRY(set_l2_window(ctx, ctx->parts[0].visited.p, nwords * sizeof(uint32_t)));
   for (auto& ev : D->ev) BFB_CUDA(cudaEventCreate(&ev));
+  if (parts > 1) {
+    D->part_ev.resize(parts + 1);
+    for (auto& ev : D->part_ev) BFB_CUDA(cudaEventCreate(&ev));
+  }
   ctx->engine_ready = true;
   return BFB_OK;
 }
@@ -1188,7 +1206,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   const int64_t nwords = (n + 31) / 32;
   const int64_t* off = ctx->g.offsets.p;
   int64_t launches = 0;
-  double t_expand = 0, t_exchange = 0, t_commit = 0;
+  double t_expand = 0, t_exchange = 0, t_commit = 0, t_expand_max = 0;
   int64_t expand_launches = 0;
 
   BFB_CUDA(cudaEventRecord(D->ev[0], s));
@@ -1225,7 +1243,9 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   while (true) {
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
     // Phase 1
+    const bool part_timing = ctx->timing && P > 1;
     for (int g = 0; g < P; ++g) {
+      if (part_timing) BFB_CUDA(cudaEventRecord(D->part_ev[g], s));
       PartView v = view_of(ctx, ctx->parts[g]);
       if (bottom_up) {
         const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo) * 32, 256, sms, 8);
@@ -1243,6 +1263,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       ++expand_launches;
     }
     if (bottom_up) ++bu_levels;
+    if (part_timing) BFB_CUDA(cudaEventRecord(D->part_ev[P], s));
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[3], s));
     // Phase 2
     if (!D->rounds.empty()) {
@@ -1289,7 +1310,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
           launches += launch_commit_count(v, off, ctx->run.p, sms, s);
       }
       if (nwords - (p.whi - p.wlo) > 0) {
-        k_commit_rest<<<small_grid, 256, 0, s>>>(v, next_level);
+        k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(v, next_level);
         ++launches;
       }
     }
@@ -1343,6 +1364,13 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       t_expand += a;
       t_exchange += b;
       t_commit += c;
+      float mx = 0;
+      for (int g = 0; part_timing && g < P; ++g) {
+        float d = 0;
+        BFB_CUDA(cudaEventElapsedTime(&d, D->part_ev[g], D->part_ev[g + 1]));
+        mx = std::max(mx, d);
+      }
+      t_expand_max += part_timing ? mx : a;
     }
     frontier = ctx->pinned[0];
     if (frontier == 0) break;
@@ -1409,6 +1437,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     st->kernel_launches = launches;
     st->edges_examined = rc.edges_examined;
     st->bottom_up_levels = bu_levels;
+    st->expand_max_part_ms = t_expand_max;
   }
   // buffer-bound check: incoming <= f * |V|
   for (auto x : hw)
@@ -1652,7 +1681,7 @@ int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
     D->launches += launch_commit(v, ctx->g.offsets.p, next_level, ctx->run.p, ctx->num_sms, s);
   }
   if (nwords - (p.whi - p.wlo) > 0) {
-    k_commit_rest<<<grid_cap(nwords, 256, ctx->num_sms, 4), 256, 0, s>>>(v, next_level);
+    k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, ctx->num_sms), 256, 0, s>>>(v, next_level);
     ++D->launches;
   }
   BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1924,7 +1953,6 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   bool bottom_up = ctx->direction == 2;
   int64_t bu_levels = 0, prev_frontier = 1, nsizes = 1, launches = 0;
   if (sizes_out && max_levels > 0) sizes_out[0] = 1;
-  const unsigned rest_grid = grid_cap(nwords, 256, sms, 4);
   double t_expand = 0, t_exchange = 0, t_commit = 0;
   int64_t expand_launches = 0;
   while (true) {
@@ -1986,7 +2014,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
         launches += launch_commit_count(v, off, ctx->run.p, sms, s);
     }
     if (nwords - (p.whi - p.wlo) > 0) {
-      k_commit_rest<<<rest_grid, 256, 0, s>>>(v, next_level);
+      k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(v, next_level);
       ++launches;
     }
     bool next_bu = ctx->direction == 2;

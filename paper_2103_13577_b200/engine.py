@@ -114,7 +114,8 @@ def stats_of(sizes, st, hw):
         reached=int(st.reached),
         exchange_bytes=int(st.exchange_bytes),
         device_ms={"total": st.elapsed_ms, "expand": st.expand_ms,
-                   "exchange": st.exchange_ms, "commit": st.commit_ms},
+                   "exchange": st.exchange_ms, "commit": st.commit_ms,
+                   "expand_max_part": st.expand_max_part_ms},
         kernel_launches=int(st.kernel_launches),
         edges_examined=int(st.edges_examined),
         bottom_up_levels=int(st.bottom_up_levels),

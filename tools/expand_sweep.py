@@ -19,12 +19,12 @@ for parents, direction in ((False, "top-down"), (True, "top-down"), (True, "opti
     dg.set_direction(direction, float(os.environ.get("SW_ALPHA", "14")), float(os.environ.get("SW_BETA", "24")))
     dg.set_timing(True)
     dg.bfs(int(roots[0]), levels=False)
-    t = []; ex = []; cm = []; xc = []
+    t = []; ex = []; cm = []; xc = []; mp = []
     for r in roots:
         _, _, sizes, st, _ = dg.bfs(int(r), levels=False)
-        t.append(st.traversed_edges / st.elapsed_ms / 1e6); ex.append(st.expand_ms); cm.append(st.commit_ms); xc.append(st.exchange_ms)
+        t.append(st.traversed_edges / st.elapsed_ms / 1e6); ex.append(st.expand_ms); cm.append(st.commit_ms); xc.append(st.exchange_ms); mp.append(st.expand_max_part_ms)
     hm = len(t) / sum(1 / x for x in t)
-    print(f"{os.environ.get('SW_TAG')}: {direction} parents={parents} hmean={hm:.1f} GTEP/s expand={sum(ex)/len(ex):.2f} ms commit={sum(cm)/len(cm):.2f} ms exchange={sum(xc)/len(xc):.2f} ms bu_levels={st.bottom_up_levels} examined={st.edges_examined}", flush=True)
+    print(f"{os.environ.get('SW_TAG')}: {direction} parents={parents} hmean={hm:.1f} GTEP/s expand={sum(ex)/len(ex):.2f} ms commit={sum(cm)/len(cm):.2f} ms exchange={sum(xc)/len(xc):.2f} ms expand_max_part={sum(mp)/len(mp):.2f} ms bu_levels={st.bottom_up_levels} examined={st.edges_examined}", flush=True)
 ''' % ROOT
 
 if __name__ == "__main__":
