@@ -146,7 +146,8 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
 // Sparse levels (fewer tiles than warps): one warp per subtile, its first
 // row found by a 32-ary warp search of q_pre inside the tile's rows, so a
 // small frontier still spreads over many warps.
-// Per edge: the adjacency word (evict-first), a probe of the visited bitmap
+// Per edge: the adjacency word (no L1 allocation, L2 evict-first), a probe
+// of the visited bitmap (default caching: its L1 hits matter)
 // and, if the probe saw the bit clear, a fire-and-forget red.or claim
 // (check-and-set).  The commit finds the new bits as
 // visited & ~start, so no claim needs the atomic's old value.
@@ -158,6 +159,21 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
 #ifndef BFB_EXPAND_MINB
 #define BFB_EXPAND_MINB 4
 #endif
+// Adjacency words are read once per BFS: no L1 allocation, evict-first in
+// L2 (createpolicy), so the streamed adjacency does not push the visited
+// bitmap out of either cache.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint32_t adj_word(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
 
 // One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
 // with rb the row holding edge r0 and ve the last row that can matter.
@@ -166,7 +182,7 @@ template <bool kParents>
 __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
                                                    const uint32_t* __restrict__ adj, int64_t r0,
                                                    int span, uint32_t rb, uint32_t ve,
-                                                   unsigned le_mask) {
+                                                   unsigned le_mask, uint64_t pol) {
   const int lane = threadIdx.x & 31;
   const uint32_t vs = rb;
   uint32_t u[kExpandItems];
@@ -194,7 +210,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
       before += __popc(M);
       const int64_t b = __shfl_sync(0xffffffffu, base, idx);
       if (r >= lo && r < cover_hi) {
-        u[it] = ld_stream_u32(adj + b + r0 + r);
+        u[it] = adj_word(adj + b + r0 + r, pol);
         done |= 1u << it;
         if (kParents) {
           const uint32_t ro = rb + idx - vs;
@@ -262,6 +278,7 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
   const unsigned le_mask = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);  // bits [0, lane]
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t pol = l2_evict_first_policy();
   if (ntiles >= nwarps) {
     for (int64_t t = gw; t < ntiles; t += nwarps) {
       const int64_t e0 = t * kTile;
@@ -270,7 +287,7 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       uint32_t cur = v.tile_vstart[t];
       for (int k = 0; k * kSub < span; ++k)
         cur = expand_subtile<kParents>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
-                                       cur, ve, le_mask);
+                                       cur, ve, le_mask, pol);
     }
   } else {
     const int64_t nsub = (T + kSub - 1) / kSub;
@@ -280,7 +297,7 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const uint32_t vs = v.tile_vstart[t];
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       const uint32_t cur = (st % kSubPerTile) ? find_row(v.q_pre, vs, ve, r0) : vs;
-      expand_subtile<kParents>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask);
+      expand_subtile<kParents>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask, pol);
     }
   }
 }
