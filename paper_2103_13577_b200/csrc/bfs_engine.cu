@@ -1,22 +1,25 @@
 // ButterFly BFS engine on device: Alg. 2.
 //
-// Per level and per node g (a "part", one per GPU in production, several per
-// GPU for testing):
-//   phase 1  k_expand        edge-balanced top-down expansion of q_local[g]
-//                            (load-balanced search over 2048-edge tiles;
-//                            visited probe + red.or claim; parent write)
+// Per level and per node g (a "part": one per GPU in production -- one
+// process per GPU, rank_bfs -- or several in one context for testing):
+//   phase 1  k_expand_w      warp-centric top-down expansion of q_local[g]
+//                            over 256-edge subtiles of 2048-edge tiles
+//                            (visited probe + red.or claim; parent store)
+//            k_bottom_up     bottom-up phase 1 (direction-optimizing levels)
 //   phase 2  per round i of the butterfly schedule:
-//            k_publish       snapshot q_global_next[g] as the bitmap
-//                            visited ^ start (round-start snapshot)
-//            k_account       RunStats accounting from the snapshot sizes
-//            k_merge         OR each scheduled source's snapshot into g's
-//                            visited bitmap (check-and-set)
-//   commit   k_commit_owned  new = visited & ~start over g's owned words:
-//                            level writes, start := visited, and the next
-//                            q_local (ascending) with its degree prefix and
-//                            tile starts, via a single-pass decoupled
-//                            look-back scan; frontier count for termination
-//            k_commit_rest   the same level/start update for the other words
+//            one context:    k_publish (snapshot q_global_next[g] as the
+//                            bitmap visited & ~start), k_account
+//                            (RunStats), k_merge (OR each scheduled source's
+//                            snapshot into g's visited bitmap)
+//            one process per node: k_publish_q, k_signal / k_wait (NVLink
+//                            mailbox barrier), k_account_mail, k_merge_queue
+//                            / k_merge_mail (sources read in peer HBM)
+//   commit   k_commit_count -> k_unit_scan_* -> k_commit_write over g's owned
+//                            words: new = visited & ~start, levels, start :=
+//                            visited, and the next q_local (ascending) with
+//                            its degree prefix and tile starts; frontier count
+//            k_commit_rest   the level/start update for the other words
+//            k_commit_light[_count]  queue-less variants for bottom-up levels
 // The synchronized frontier is the bitmap difference; the queue form of
 // q_global is never materialised, so no queue-append atomics exist.
 #include <algorithm>
@@ -1031,29 +1034,6 @@ struct EngineTables {
   }
 };
 
-// L2 persistence window over the visited bitmap (BFB_L2_PERSIST=1): the
-// random probes then hit a bitmap that the streaming adjacency reads
-// (evict-first) cannot push out of the 126 MB L2.
-static int set_l2_window(bfb_ctx* ctx, void* base, size_t bytes) {
-  const char* e = std::getenv("BFB_L2_PERSIST");
-  if (!e || std::atoi(e) == 0) return BFB_OK;
-  int max_persist = 0, max_window = 0;
-  BFB_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
-  BFB_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
-  if (max_persist <= 0 || max_window <= 0) return BFB_OK;
-  const size_t carve = std::min(bytes, (size_t)max_persist);
-  BFB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
-  cudaStreamAttrValue attr = {};
-  attr.accessPolicyWindow.base_ptr = base;
-  attr.accessPolicyWindow.num_bytes = std::min(bytes, (size_t)max_window);
-  attr.accessPolicyWindow.hitRatio =
-      std::min(1.0f, (float)carve / (float)attr.accessPolicyWindow.num_bytes);
-  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  BFB_CUDA(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &attr));
-  return BFB_OK;
-}
-
 void engine_release(bfb_ctx* ctx) {
   ctx->parts.clear();
   ctx->run.release();
@@ -1188,18 +1168,7 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_TRY(expand_occupancy<true>(&occ));
   else
     BFB_TRY(expand_occupancy<false>(&occ));
-  // Developer knobs for tuning runs: cap resident expand blocks per SM, and
-  // the expand's shared-memory carveout in percent (it uses none; unset =
-  // driver default).
-  if (const char* e = std::getenv("BFB_EXPAND_OCC")) occ = std::min(occ, std::max(1, std::atoi(e)));
-  if (const char* e = std::getenv("BFB_CARVEOUT")) {
-    const int pct = std::atoi(e);
-    BFB_CUDA(cudaFuncSetAttribute(k_expand_w<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    BFB_CUDA(cudaFuncSetAttribute(k_expand_w<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-  }
-
   ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
-  BFB_TRY(set_l2_window(ctx, ctx->parts[0].visited.p, nwords * sizeof(uint32_t)));
   for (auto& ev : D->ev) BFB_CUDA(cudaEventCreate(&ev));
   if (parts > 1) {
     D->part_ev.resize(parts + 1);
