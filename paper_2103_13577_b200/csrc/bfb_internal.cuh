@@ -175,6 +175,7 @@ struct Part {
   DevBuf<uint32_t> pub_alt;        // odd-round snapshot (multi-process mode)
   DevBuf<uint32_t> pub_q;          // queue-form snapshots, 2 x nwords entries (by parity)
   DevBuf<uint32_t> front;          // level-L frontier bitmap (bottom-up phase 1)
+  DevBuf<uint32_t> lvbits;         // per level 1..kLevelBits-1: that level's new-vertex bitmap
   DevBuf<uint32_t> q_v;            // q_local vertex ids, ascending
   DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local
   DevBuf<int64_t> q_base;          // offsets[v] - q_pre (adjacency base per row)

@@ -43,6 +43,11 @@ constexpr int kScanItems = 16;                 // commit unit scan: units per th
 constexpr int64_t kScanTile = 256 * kScanItems;
 constexpr int64_t kWordPad = 1024;  // bitmap allocation padding (words)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+// d_local is materialised once at termination from per-level new-vertex
+// bitmaps (one dense 4-byte word per 32 vertices per level, instead of a
+// scattered 4-byte store per discovered vertex); levels from kLevelBits on
+// (high-diameter graphs) are written directly.
+constexpr int kLevelBits = 32;
 
 struct PartView {
   int64_t lo, hi, wlo, whi, nwords;
@@ -52,6 +57,8 @@ struct PartView {
   uint32_t* parent;
   uint32_t* pub;
   uint32_t* front;  // level-L frontier bitmap, written at commit when direction != 0
+  uint32_t* lvbits; // commit: this level's new-vertex bitmap (levels materialised at the end),
+                    // nullptr = write d_local directly (levels >= kLevelBits)
   uint32_t* q_v;
   int64_t* q_pre;
   int64_t* q_base;  // offsets[v] - q_pre: adjacency index = q_base + edge prefix
@@ -79,6 +86,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.parent = p.parent.p;
   v.pub = p.pub.p;
   v.front = ctx->direction ? p.front.p : nullptr;
+  v.lvbits = nullptr;
   v.q_v = p.q_v.p;
   v.q_pre = p.q_pre.p;
   v.q_base = p.q_base.p;
@@ -97,6 +105,15 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.off = ctx->g.offsets.p;
   v.nonisol = ctx->g.nonisol.p;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
+  return v;
+}
+
+// PartView for the commit of level next_level: new-vertex bitmap slot of
+// that level (nullptr past kLevelBits: direct d_local writes).
+PartView commit_view_of(bfb_ctx* ctx, Part& p, uint32_t next_level) {
+  PartView v = view_of(ctx, p);
+  const int64_t pad = (int64_t)(p.lvbits.n / kLevelBits);
+  v.lvbits = next_level < (uint32_t)kLevelBits ? p.lvbits.p + (int64_t)next_level * pad : nullptr;
   return v;
 }
 
@@ -458,6 +475,10 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
     if (!v.rebuild) fr += __popc(nb);  // a rebuild's frontier was counted by its level's commit
+    if (v.lvbits && !v.rebuild) {
+      const int64_t w = v.abase + unit * 32 + lane;
+      if (w >= v.wlo && w < v.whi) v.lvbits[w] = nb;
+    }
     const uint32_t c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(own));
     int64_t d = 0;
     if (c) d = warp_sum_i64(word_degree_sum(own, (v.abase + unit * 32 + lane) << 5, off));
@@ -596,7 +617,7 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
     unsigned m = __ballot_sync(0xffffffffu, nb != 0);
     if (!m) continue;
     const int64_t w0 = v.abase + unit * 32;
-    while (m && !v.rebuild) {
+    while (m && !v.rebuild && !v.lvbits) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
@@ -668,10 +689,11 @@ __global__ void __launch_bounds__(256) k_commit_light_count(PartView v, const in
   for (int64_t unit = gw; unit < v.nunits; unit += nw) {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
+    const int64_t w0 = v.abase + unit * 32;
+    if (v.lvbits && w0 + lane >= v.wlo && w0 + lane < v.whi) v.lvbits[w0 + lane] = nb;
     unsigned m = __ballot_sync(0xffffffffu, nb != 0);
     if (!m) continue;
-    const int64_t w0 = v.abase + unit * 32;
-    while (m) {
+    while (m && !v.lvbits) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
@@ -713,7 +735,7 @@ __global__ void __launch_bounds__(256) k_commit_light(PartView v, uint32_t next_
     unsigned m = __ballot_sync(0xffffffffu, nb != 0);
     if (!m) continue;
     const int64_t w0 = v.abase + unit * 32;
-    while (m) {
+    while (m && !v.lvbits) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
@@ -743,9 +765,10 @@ __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_l
     const bool in = i < span;
     const uint32_t a = in ? v.visited[w] : 0u;
     const uint32_t nb = a & ~(in ? v.start[w] : 0u);
+    if (v.lvbits && in) v.lvbits[w] = nb;
     unsigned m = __ballot_sync(0xffffffffu, nb != 0);
     if (!m) continue;
-    while (m) {
+    while (m && !v.lvbits) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
       const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
@@ -816,6 +839,74 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
   }
   ex = (unsigned long long)warp_sum_i64((int64_t)ex);
   if (lane == 0 && ex) atomicAdd(examined, ex);
+}
+
+// d_local at termination: vertex u gets the level l in
+// [1, nl] whose new-vertex bitmap holds it; otherwise, if visited, the value
+// already in d_local (the root's 0, or a level >= kLevelBits written
+// directly); otherwise UNREACHED.  Warp = 32 consecutive words: lane k loads
+// word k of every level bitmap (coalesced, all in flight at once) and folds
+// them into bit slices of the level index, then lanes take 4 vertices each
+// (shuffles) and write d_local with 16-byte stores, 512 contiguous bytes per
+// warp store.
+__global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __restrict__ lvbits,
+                                                          int64_t pad, int nl,
+                                                          const uint32_t* __restrict__ visited,
+                                                          uint32_t* __restrict__ level, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t nunits = (nwords + 31) / 32;
+  for (int64_t unit = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; unit < nunits;
+       unit += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t w0 = unit * 32;
+    const int64_t wk = w0 + lane;
+    const bool in = wk < nwords;
+    // The level bitmaps are disjoint, so a vertex's level l is the OR of the
+    // bitmaps' indices: bit-slice it into five words (bit k of l for each of
+    // this word's 32 vertices) plus "in some bitmap".
+    uint32_t slice[5] = {0u, 0u, 0u, 0u, 0u}, any = 0u;
+#pragma unroll
+    for (int l = 1; l < kLevelBits; ++l) {
+      const uint32_t x = (l <= nl && in) ? __ldg(lvbits + l * pad + wk) : 0u;
+      any |= x;
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+        if ((l >> k) & 1) slice[k] |= x;
+    }
+    const uint32_t vis = in ? __ldg(visited + wk) : 0u;
+    // 8 passes of 128 vertices: lane = 4 consecutive vertices of word
+    // q * 4 + lane / 8, one 16-byte store each (a warp writes 512 contiguous
+    // bytes per pass)
+    const int sub = lane >> 3, b0 = (lane & 7) * 4;
+#pragma unroll 2
+    for (int q = 0; q < 8; ++q) {
+      const int j = q * 4 + sub;
+      uint32_t sl[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) sl[k] = __shfl_sync(0xffffffffu, slice[k], j) >> b0;
+      const uint32_t aj = __shfl_sync(0xffffffffu, any, j) >> b0;
+      const uint32_t vj = __shfl_sync(0xffffffffu, vis, j) >> b0;
+      const int64_t u0 = ((w0 + j) << 5) + b0;
+      if (u0 >= n) continue;
+      uint32_t lv[4];
+      bool keep = false;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        uint32_t l = 0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) l |= ((sl[k] >> t) & 1u) << k;
+        const bool found = (aj >> t) & 1u, seen = (vj >> t) & 1u;
+        lv[t] = found ? l : kNone;
+        keep |= !found && seen;
+      }
+      if (u0 + 4 <= n && !keep) {
+        *reinterpret_cast<uint4*>(level + u0) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+      } else {
+        for (int t = 0; t < 4 && u0 + t < n; ++t)
+          if (((aj >> t) & 1u) || !((vj >> t) & 1u)) level[u0 + t] = lv[t];
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------ outputs ----
@@ -920,6 +1011,17 @@ unsigned grid_cap(int64_t work, int block, int num_sms, int per_sm = 8) {
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (unsigned)g;
+}
+
+// d_local from the level bitmaps at termination (last_level = the deepest
+// level committed); returns kernels launched.
+int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStream_t s) {
+  const int64_t pad = (int64_t)(p.lvbits.n / kLevelBits);
+  const int nl = (int)std::min<int64_t>(last_level, kLevelBits - 1);
+  k_levels_from_bits<<<resident_grid(k_levels_from_bits, (ctx->g.n + 31) / 32, 256,
+                                     ctx->num_sms),
+                       256, 0, s>>>(p.lvbits.p, pad, nl, p.visited.p, p.level.p, ctx->g.n);
+  return 1;
 }
 
 // Multi-process merge: OR the round's source snapshots (peer memory mapped
@@ -1106,6 +1208,7 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
     BFB_TRY(p.q_base.alloc(owned + 1));
     BFB_TRY(p.tile_vstart.alloc(p.tile_cap));
     BFB_TRY(p.front.alloc(nwords_pad));
+    BFB_TRY(p.lvbits.alloc((size_t)kLevelBits * nwords_pad));
     {
       const int64_t nunits = (p.whi - (p.wlo & ~(int64_t)31) + 31) / 32 + 1;
       const int64_t ntiles = (nunits + kScanTile - 1) / kScanTile + 1;
@@ -1206,7 +1309,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     Part& p = ctx->parts[g];
     BFB_CUDA(cudaMemsetAsync(p.visited.p, 0, nwords * sizeof(uint32_t), s));
     BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
-    BFB_CUDA(cudaMemsetAsync(p.level.p, 0xFF, n * sizeof(uint32_t), s));
+    // (d_local needs no reset: it is materialised at termination)
     if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
     if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
     k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), off, root, g == owner ? 1 : 0, ctx->run.p);
@@ -1288,7 +1391,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     const bool light = ctx->direction != 0 && bottom_up;
     for (int g = 0; g < P; ++g) {
       Part& p = ctx->parts[g];
-      PartView v = view_of(ctx, p);
+      PartView v = commit_view_of(ctx, p, next_level);
       if (p.whi > p.wlo) {
         if (light)
           launches += launch_commit_light_count(v, off, next_level, ctx->run.p, sms, s);
@@ -1331,9 +1434,11 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       if (p.whi <= p.wlo) continue;
       if (light) {
         if (!next_bu)
-          launches += launch_commit_rebuild(view_of(ctx, p), off, next_level, ctx->run.p, sms, s);
+          launches += launch_commit_rebuild(commit_view_of(ctx, p, next_level), off, next_level,
+                                            ctx->run.p, sms, s);
       } else {
-        launches += launch_commit_write(view_of(ctx, p), off, next_level, !next_bu, sms, s);
+        launches += launch_commit_write(commit_view_of(ctx, p, next_level), off, next_level,
+                                        !next_bu, sms, s);
       }
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
@@ -1369,6 +1474,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     ++level;
     if (level > n) return fail(BFB_ERR_CAPACITY, "level count exceeded |V| (internal error)");
   }
+  for (int g = 0; g < P; ++g) launches += launch_materialise_levels(ctx, ctx->parts[g], level + 1, s);
   BFB_CUDA(cudaEventRecord(D->ev[1], s));
   // Parents of the output view: any node's phase-1 claim is a valid parent.
   const uint32_t* parents_dev = nullptr;
@@ -1584,7 +1690,6 @@ int rank_begin(bfb_ctx* ctx, int64_t root) {
   BFB_CUDA(cudaMemsetAsync(ctx->run.p, 0, sizeof(RunCounters), s));
   BFB_CUDA(cudaMemsetAsync(p.visited.p, 0, nwords * sizeof(uint32_t), s));
   BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
-  BFB_CUDA(cudaMemsetAsync(p.level.p, 0xFF, n * sizeof(uint32_t), s));
   if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
   if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
   const int owner = root >= p.lo && root < p.hi;
@@ -1658,9 +1763,9 @@ int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
   EngineTables* D = ctx->tables;
   cudaStream_t s = ctx->stream;
   Part& p = ctx->parts[0];
-  PartView v = view_of(ctx, p);
   const int64_t nwords = (ctx->g.n + 31) / 32;
   const uint32_t next_level = (uint32_t)(D->level + 1);
+  PartView v = commit_view_of(ctx, p, next_level);
   k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
   ++D->launches;
   if (p.whi > p.wlo) {
@@ -1688,6 +1793,7 @@ int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
 int rank_finish(bfb_ctx* ctx, bfb_run_stats* st) {
   EngineTables* D = ctx->tables;
   cudaStream_t s = ctx->stream;
+  D->launches += launch_materialise_levels(ctx, ctx->parts[0], D->level + 1, s);
   BFB_CUDA(cudaEventRecord(D->ev[1], s));
   RunCounters rc;
   BFB_CUDA(cudaMemcpyAsync(&rc, ctx->run.p, sizeof(rc), cudaMemcpyDeviceToHost, s));
@@ -1989,18 +2095,19 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[4], s));
     // commit: count pass, direction decision, write pass (as engine_bfs)
     const uint32_t next_level = (uint32_t)(D->level + 1);
+    const PartView cv = commit_view_of(ctx, p, next_level);
     k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
     ++launches;
     if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
     const bool light = ctx->direction != 0 && bottom_up;
     if (p.whi > p.wlo) {
       if (light)
-        launches += launch_commit_light_count(v, off, next_level, ctx->run.p, sms, s);
+        launches += launch_commit_light_count(cv, off, next_level, ctx->run.p, sms, s);
       else
-        launches += launch_commit_count(v, off, ctx->run.p, sms, s);
+        launches += launch_commit_count(cv, off, ctx->run.p, sms, s);
     }
     if (nwords - (p.whi - p.wlo) > 0) {
-      k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(v, next_level);
+      k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(cv, next_level);
       ++launches;
     }
     bool next_bu = ctx->direction == 2;
@@ -2022,9 +2129,9 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     if (p.whi > p.wlo) {
       if (light) {
         if (!next_bu)
-          launches += launch_commit_rebuild(v, off, next_level, ctx->run.p, sms, s);
+          launches += launch_commit_rebuild(cv, off, next_level, ctx->run.p, sms, s);
       } else {
-        launches += launch_commit_write(v, off, next_level, !next_bu, sms, s);
+        launches += launch_commit_write(cv, off, next_level, !next_bu, sms, s);
       }
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));

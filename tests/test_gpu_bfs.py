@@ -278,3 +278,23 @@ def test_config4_s28_ef8_fanout_sweep():
         assert st.rounds_executed == len(sizes) * rounds
         assert st.remote_messages <= len(sizes) * 8 * 7
         assert dg.validate(r) == 0
+
+
+@pytest.mark.parametrize("cn", [1, 3])
+def test_deep_graph_levels_past_the_level_bitmaps(cn):
+    """Levels 0..31 are materialised from per-level bitmaps at termination,
+    deeper ones written directly (kLevelBits = 32): a 300-vertex path plus a
+    cycle and an isolated vertex, from both ends and the middle, all parts,
+    parents on, in every phase-1 direction."""
+    edges = [(i, i + 1) for i in range(299)] + [(300, 301), (301, 302), (302, 300)]
+    off, adj = util.csr_of_undirected(304, edges)
+    g = _g(off, adj)
+    p = graphs.partition_1d(g, cn)
+    for direction in ("top-down", "optimizing", "bottom-up"):
+        for root in (0, 150, 299, 301, 303):
+            cfg = engine.EngineConfig(fanout=1, parents=True, direction=direction)
+            d, st = engine.run(g, p, root, cfg)
+            ref = ob.bfs_top_down(off, adj, root)
+            assert np.array_equal(d.d, ref), (cn, direction, root)
+            assert not ov.check_parents(off, adj, root, d.d, d.parents)
+            assert st.per_level_frontier_size == ob.level_sizes(ref)
