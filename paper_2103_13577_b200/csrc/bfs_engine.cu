@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_l
 // so levels, frontier sizes and traversed edges are identical to
 // top-down.  Warp = one bitmap word (32 consecutive vertices); each lane
 // checks kBuBatch neighbours per round trip.
-constexpr int kBuBatch = 4;
+constexpr int kBuBatch = 2;  // measured: 1 -> 607, 2 -> 611, 4 -> 554, 8 -> 455 GTEP/s (s29 DO)
 
 template <bool kParents>
 __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* __restrict__ adj,
