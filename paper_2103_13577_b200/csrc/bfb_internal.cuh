@@ -138,6 +138,7 @@ struct DevGraph {
   DevBuf<int64_t> offsets;   // n+1
   DevBuf<uint32_t> adj;      // m
   DevBuf<uint32_t> nonisol;  // bitmap of degree > 0 (bottom-up candidates), built at engine setup
+  DevBuf<uint16_t> deg16;    // min(degree, 65535) per vertex (commit degree sums), engine setup
   bool valid = false;
 };
 

@@ -70,6 +70,7 @@ struct PartView {
   PartCounters* ctr;
   const int64_t* off;  // CSR offsets (rows of q_v)
   const uint32_t* nonisol;  // degree > 0 bitmap
+  const uint16_t* deg16;    // min(degree, 65535)
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
@@ -104,6 +105,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.ctr = p.ctr.p;
   v.off = ctx->g.offsets.p;
   v.nonisol = ctx->g.nonisol.p;
+  v.deg16 = ctx->g.deg16.p;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -442,26 +444,43 @@ __device__ __forceinline__ void unit_word(const PartView& v, int64_t unit, int l
   own = nb & owned_mask(w, v.lo, v.hi);
 }
 
-// Degree sum of the vertices whose bits are set in x (vertex ids vbase + bit),
-// four bits per step so eight offsets loads are in flight at once.
-__device__ __forceinline__ int64_t word_degree_sum(uint32_t x, int64_t vbase,
-                                                   const int64_t* __restrict__ off) {
+// Degree sum of the vertices whose bits are set in x (word w: vertices
+// 32w..32w+31) from the 16-bit degree table: the word's 32 degrees are four
+// 16-byte loads (a warp reads its unit's 2 KB contiguously); degrees >= 65535
+// come from the offsets.
+__device__ __forceinline__ int64_t word_degree_sum16(uint32_t x, int64_t w,
+                                                     const uint16_t* __restrict__ deg16,
+                                                     const int64_t* __restrict__ off) {
+  if (!x) return 0;
+  const uint4* p = reinterpret_cast<const uint4*>(deg16 + (w << 5));
+  uint32_t q[16];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 t = __ldg(p + k);
+    q[4 * k] = t.x;
+    q[4 * k + 1] = t.y;
+    q[4 * k + 2] = t.z;
+    q[4 * k + 3] = t.w;
+  }
   int64_t d = 0;
-  while (x) {
-    int b[4];
+  bool esc = false;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      b[k] = x ? __ffs(x) - 1 : -1;
-      x &= x - 1;
+  for (int b = 0; b < 32; ++b) {
+    const uint32_t db = (q[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu;
+    if ((x >> b) & 1u) {
+      d += db;
+      esc |= db == 0xFFFFu;
     }
-    int64_t lo[4], hi[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      lo[k] = b[k] >= 0 ? __ldg(off + vbase + b[k]) : 0;
-      hi[k] = b[k] >= 0 ? __ldg(off + vbase + b[k] + 1) : 0;
+  }
+  if (esc) {  // a hub: recount its exact degree
+#pragma unroll 1
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t db = (q[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu;
+      if (((x >> b) & 1u) && db == 0xFFFFu) {
+        const int64_t u = (w << 5) + b;
+        d += (__ldg(off + u + 1) - __ldg(off + u)) - 0xFFFF;
+      }
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) d += hi[k] - lo[k];
   }
   return d;
 }
@@ -481,7 +500,7 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
     }
     const uint32_t c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(own));
     int64_t d = 0;
-    if (c) d = warp_sum_i64(word_degree_sum(own, (v.abase + unit * 32 + lane) << 5, off));
+    if (c) d = warp_sum_i64(word_degree_sum16(own, v.abase + unit * 32 + lane, v.deg16, off));
     if (lane == 0) {
       v.ucnt[unit] = c;
       v.udeg[unit] = d;
@@ -706,7 +725,7 @@ __global__ void __launch_bounds__(256) k_commit_light_count(PartView v, const in
     }
     if (own) {
       qc += __popc(own);
-      qe += word_degree_sum(own, (w0 + lane) << 5, off);
+      qe += word_degree_sum16(own, w0 + lane, v.deg16, off);
     }
   }
   __shared__ int64_t red[32];
@@ -920,15 +939,18 @@ __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n
 }
 
 // Bitmap of vertices with degree > 0 (lane = vertex, ballot per word).
-__global__ void k_nonisolated(const int64_t* __restrict__ off, int64_t n, uint32_t* out,
-                              int64_t nwords_pad) {
+// Per-vertex tables built once per engine setup (lane = vertex): the bitmap
+// of degree > 0 and min(degree, 65535) as 16 bits.
+__global__ void k_vertex_tables(const int64_t* __restrict__ off, int64_t n, uint32_t* nonisol,
+                                uint16_t* deg16, int64_t nwords_pad) {
   const int lane = threadIdx.x & 31;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords_pad;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t u = (w << 5) + lane;
-    const bool has = u < n && __ldg(off + u + 1) > __ldg(off + u);
-    const unsigned b = __ballot_sync(0xffffffffu, has);
-    if (lane == 0) out[w] = b;
+    const int64_t d = u < n ? __ldg(off + u + 1) - __ldg(off + u) : 0;
+    const unsigned b = __ballot_sync(0xffffffffu, d > 0);
+    if (lane == 0) nonisol[w] = b;
+    deg16[u] = (uint16_t)min(d, (int64_t)0xFFFF);
   }
 }
 
@@ -1182,8 +1204,9 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
                           cudaMemcpyDeviceToHost));
   }
   BFB_TRY(ctx->g.nonisol.alloc(nwords_pad));
-  k_nonisolated<<<grid_cap(nwords_pad * 32, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
-      ctx->g.offsets.p, n, ctx->g.nonisol.p, nwords_pad);
+  BFB_TRY(ctx->g.deg16.alloc((size_t)nwords_pad * 32));
+  k_vertex_tables<<<grid_cap(nwords_pad * 32, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
+      ctx->g.offsets.p, n, ctx->g.nonisol.p, ctx->g.deg16.p, nwords_pad);
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->parts.resize(parts);
   std::vector<uint32_t*> pubs(parts), viss(parts), pars(parts);
