@@ -954,6 +954,16 @@ __global__ void k_vertex_tables(const int64_t* __restrict__ off, int64_t n, uint
   }
 }
 
+// Single-node runs skip the 2 GB parent reset: every reached vertex but the
+// root gets its parent from its own claim, so only unreached vertices hold
+// stale values -- cleared here, from d_local, when parents are read out.
+__global__ void k_mask_parents(const uint32_t* __restrict__ level, uint32_t* __restrict__ parent,
+                               int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (level[i] == kNone) parent[i] = kNone;
+}
+
 // Certificate + parent validity, warp per vertex.
 __global__ void k_validate(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                            int64_t n, const uint32_t* __restrict__ level,
@@ -1333,7 +1343,10 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     BFB_CUDA(cudaMemsetAsync(p.visited.p, 0, nwords * sizeof(uint32_t), s));
     BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
     // (d_local needs no reset: it is materialised at termination)
-    if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
+    // parents: a multi-node run takes the min over nodes, so non-claimed
+    // entries must read kNone; a single node masks at read-out instead
+    if (ctx->want_parents && P > 1)
+      BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
     if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
     k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), off, root, g == owner ? 1 : 0, ctx->run.p);
     ++launches;
@@ -1524,8 +1537,12 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   BFB_CUDA(cudaEventElapsedTime(&elapsed, D->ev[0], D->ev[1]));
   if (parents_out) {
     if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
+    if (P == 1)
+      k_mask_parents<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(ctx->parts[0].level.p,
+                                                              ctx->parts[0].parent.p, n);
     std::vector<uint32_t> tmp(n);
-    BFB_CUDA(cudaMemcpy(tmp.data(), parents_dev, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    BFB_CUDA(cudaMemcpyAsync(tmp.data(), parents_dev, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
     for (int64_t i = 0; i < n; ++i) parents_out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
   }
   if (hw_out) std::memcpy(hw_out, hw.data(), P * sizeof(int64_t));
@@ -1568,11 +1585,26 @@ int engine_copy_levels(bfb_ctx* ctx, uint32_t* out) {
   return BFB_OK;
 }
 
+// Device array of the last run's output parents (kNone where unreached).
+static int output_parents(bfb_ctx* ctx, const uint32_t** out) {
+  EngineTables* D = ctx->tables;
+  if (ctx->num_parts > 1) {
+    *out = D->parents_final.p;
+    return BFB_OK;
+  }
+  Part& p = ctx->parts[0];
+  k_mask_parents<<<grid_cap(ctx->g.n, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
+      p.level.p, p.parent.p, ctx->g.n);
+  BFB_CUDA(cudaGetLastError());
+  *out = p.parent.p;
+  return BFB_OK;
+}
+
 int engine_copy_parents(bfb_ctx* ctx, int64_t* out) {
   if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
   if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
-  EngineTables* D = ctx->tables;
-  const uint32_t* src = ctx->num_parts == 1 ? ctx->parts[0].parent.p : D->parents_final.p;
+  const uint32_t* src = nullptr;
+  BFB_TRY(output_parents(ctx, &src));
   std::vector<uint32_t> tmp(ctx->g.n);
   BFB_CUDA(cudaMemcpy(tmp.data(), src, ctx->g.n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < ctx->g.n; ++i) out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
@@ -1581,9 +1613,8 @@ int engine_copy_parents(bfb_ctx* ctx, int64_t* out) {
 
 int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs) {
   if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
-  EngineTables* D = ctx->tables;
   const uint32_t* par = nullptr;
-  if (ctx->want_parents) par = ctx->num_parts == 1 ? ctx->parts[0].parent.p : D->parents_final.p;
+  if (ctx->want_parents) BFB_TRY(output_parents(ctx, &par));
   DevBuf<unsigned> err;
   BFB_TRY(err.alloc(1));
   BFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(unsigned), ctx->stream));
