@@ -361,7 +361,7 @@ def main_rank(args, cfg):
             eng.node.bfs(int(roots[(K + i) % len(roots)]))
         comm.barrier()
         out = {"teps": [], "edges": [], "t": [], "launches": 0, "expand": 0.0, "exchange": 0.0,
-               "commit": 0.0, "bu": 0, "reached": 0}
+               "commit": 0.0, "bu": 0, "reached": 0, "nvl_rate": [], "nvl_bytes": 0}
         dg.timer_start()
         for i in range(K):
             sizes, st = eng.node.bfs(int(roots[i % len(roots)]))
@@ -373,6 +373,11 @@ def main_rank(args, cfg):
             out["launches"] += int(st.kernel_launches)
             out["expand"] += comm.allreduce(float(st.expand_ms), "max")
             out["exchange"] += comm.allreduce(float(st.exchange_ms), "max")
+            # NVLink payload this rank pulled (queue or bitmap snapshots) and
+            # its own exchange time; the rate is max over ranks
+            out["nvl_rate"].append(comm.allreduce(
+                float(st.exchange_bytes) / max(1e-9, float(st.exchange_ms) * 1e-3), "max"))
+            out["nvl_bytes"] += int(comm.allreduce(int(st.exchange_bytes), "max"))
             out["commit"] += comm.allreduce(float(st.commit_ms), "max")
             out["bu"] += int(st.bottom_up_levels)
             out["reached"] += sum(sizes)
@@ -429,6 +434,14 @@ def main_rank(args, cfg):
         "clocks": clk.summary(),
         "exchange": "device-synchronised butterfly: per round publish -> NVLink mailbox signal "
                     "-> spin-wait -> in-place merge of the sources' snapshot bitmaps (CUDA IPC)",
+        "roofline_nvlink": {"bound": "nvlink", "unit": "GB/s", "peak": 900.0,
+                            "achieved": round(float(np.mean(td["nvl_rate"])) / 1e9, 1),
+                            "frac": round(float(np.mean(td["nvl_rate"])) / 900e9, 4),
+                            "bytes_per_bfs_max_rank": td["nvl_bytes"] // K,
+                            "def": "per rank: snapshot bytes pulled from peers (4 B per queued "
+                                   "vertex or n/8 B per bitmap) / that rank's phase-2 time "
+                                   "(publish + barrier + merge), max over ranks, mean over "
+                                   "BFS; peak = NVLink 5 per direction per GPU (nominal)"},
         "direction_optimizing": {"value": round(hmean(do["teps"]), 3), "unit": UNIT,
                                  "bfs_ms_mean": round(float(np.mean(do["t"])), 4),
                                  "bottom_up_levels_mean_per_rank": round(do["bu"] / K, 2)},
