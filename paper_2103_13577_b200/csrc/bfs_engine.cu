@@ -71,6 +71,7 @@ struct PartView {
   const int64_t* off;  // CSR offsets (rows of q_v)
   const uint32_t* nonisol;  // degree > 0 bitmap
   const uint16_t* deg16;    // min(degree, 65535)
+  const uint32_t* first_nbr;  // lowest-id neighbour
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
@@ -106,6 +107,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.off = ctx->g.offsets.p;
   v.nonisol = ctx->g.nonisol.p;
   v.deg16 = ctx->g.deg16.p;
+  v.first_nbr = ctx->g.first_nbr.p;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -831,7 +833,18 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
     bool found = false;
     uint32_t par = 0;
     if ((cand >> lane) & 1u) {
-      const int64_t b = __ldg(v.off + u), e = __ldg(v.off + u + 1);
+      // the lowest-id neighbour (a hub, on Kronecker graphs) decides most
+      // candidates: read it from the per-vertex table (coalesced across the
+      // warp) before touching the offsets and the row
+      const uint32_t f = __ldg(v.first_nbr + u);
+      ++ex;
+      if ((front[f >> 5] >> (f & 31)) & 1u) {
+        found = true;
+        par = f;
+      }
+    }
+    if (((cand >> lane) & 1u) && !found && __ldg(v.deg16 + u) != 1) {
+      const int64_t b = __ldg(v.off + u) + 1, e = __ldg(v.off + u + 1);
       for (int64_t j = b; j < e && !found; j += kBuBatch) {
         uint32_t p[kBuBatch];
         bool hit[kBuBatch];
@@ -941,16 +954,19 @@ __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n
 // Bitmap of vertices with degree > 0 (lane = vertex, ballot per word).
 // Per-vertex tables built once per engine setup (lane = vertex): the bitmap
 // of degree > 0 and min(degree, 65535) as 16 bits.
-__global__ void k_vertex_tables(const int64_t* __restrict__ off, int64_t n, uint32_t* nonisol,
-                                uint16_t* deg16, int64_t nwords_pad) {
+__global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                                int64_t n, uint32_t* nonisol, uint16_t* deg16, uint32_t* first_nbr,
+                                int64_t nwords_pad) {
   const int lane = threadIdx.x & 31;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords_pad;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t u = (w << 5) + lane;
-    const int64_t d = u < n ? __ldg(off + u + 1) - __ldg(off + u) : 0;
+    const int64_t o = u < n ? __ldg(off + u) : 0;
+    const int64_t d = u < n ? __ldg(off + u + 1) - o : 0;
     const unsigned b = __ballot_sync(0xffffffffu, d > 0);
     if (lane == 0) nonisol[w] = b;
     deg16[u] = (uint16_t)min(d, (int64_t)0xFFFF);
+    first_nbr[u] = d > 0 ? __ldg(adj + o) : kNone;
   }
 }
 
@@ -1215,8 +1231,10 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
   }
   BFB_TRY(ctx->g.nonisol.alloc(nwords_pad));
   BFB_TRY(ctx->g.deg16.alloc((size_t)nwords_pad * 32));
+  BFB_TRY(ctx->g.first_nbr.alloc((size_t)nwords_pad * 32));
   k_vertex_tables<<<grid_cap(nwords_pad * 32, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
-      ctx->g.offsets.p, n, ctx->g.nonisol.p, ctx->g.deg16.p, nwords_pad);
+      ctx->g.offsets.p, ctx->g.adj.p, n, ctx->g.nonisol.p, ctx->g.deg16.p, ctx->g.first_nbr.p,
+      nwords_pad);
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->parts.resize(parts);
   std::vector<uint32_t*> pubs(parts), viss(parts), pars(parts);
