@@ -832,19 +832,22 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
     const int64_t u = (w << 5) + lane;
     bool found = false;
     uint32_t par = 0;
-    if ((cand >> lane) & 1u) {
+    const bool is_cand = (cand >> lane) & 1u;
+    int64_t b = 0, e = 0;
+    if (is_cand) {
       // the lowest-id neighbour (a hub, on Kronecker graphs) decides most
       // candidates: read it from the per-vertex table (coalesced across the
-      // warp) before touching the offsets and the row
+      // warp); the row bounds are fetched alongside, not after it
       const uint32_t f = __ldg(v.first_nbr + u);
+      b = __ldg(v.off + u) + 1;
+      e = __ldg(v.off + u + 1);
       ++ex;
       if ((front[f >> 5] >> (f & 31)) & 1u) {
         found = true;
         par = f;
       }
     }
-    if (((cand >> lane) & 1u) && !found && __ldg(v.deg16 + u) != 1) {
-      const int64_t b = __ldg(v.off + u) + 1, e = __ldg(v.off + u + 1);
+    if (is_cand && !found) {
       for (int64_t j = b; j < e && !found; j += kBuBatch) {
         uint32_t p[kBuBatch];
         bool hit[kBuBatch];
