@@ -813,8 +813,11 @@ __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_l
 // neighbour in the level-L frontier bitmap and claims itself on the first hit.
 // Discoveries are owned vertices only; phase 2 and the commit are unchanged,
 // so levels, frontier sizes and traversed edges are identical to
-// top-down.  Warp = one bitmap word (32 consecutive vertices); each lane
-// checks kBuBatch neighbours per round trip.
+// top-down.  A warp takes 32 bitmap words at a time (one coalesced load of
+// their visited / non-isolated bits), then walks the words that have
+// candidates with lane = vertex: first the vertex's lowest-id neighbour from
+// a per-vertex table, then the rest of its row, kBuBatch neighbours per
+// round trip.
 constexpr int kBuBatch = 2;  // measured: 1 -> 607, 2 -> 611, 4 -> 554, 8 -> 455 GTEP/s (s29 DO)
 
 template <bool kParents>
@@ -825,52 +828,60 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t* __restrict__ front = v.front;
   unsigned long long ex = 0;
-  for (int64_t w = v.wlo + gw; w < v.whi; w += nw) {
-    const uint32_t vis = v.visited[w];
-    const uint32_t cand = owned_mask(w, v.lo, v.hi) & ~vis & v.nonisol[w];
-    if (!cand) continue;
-    const int64_t u = (w << 5) + lane;
-    bool found = false;
-    uint32_t par = 0;
-    const bool is_cand = (cand >> lane) & 1u;
-    int64_t b = 0, e = 0;
-    if (is_cand) {
-      // the lowest-id neighbour (a hub, on Kronecker graphs) decides most
-      // candidates: read it from the per-vertex table (coalesced across the
-      // warp); the row bounds are fetched alongside, not after it
-      const uint32_t f = __ldg(v.first_nbr + u);
-      b = __ldg(v.off + u) + 1;
-      e = __ldg(v.off + u + 1);
-      ++ex;
-      if ((front[f >> 5] >> (f & 31)) & 1u) {
-        found = true;
-        par = f;
+  // 32 words per step: lane k reads word k's visited / non-isolated bits
+  // (one coalesced load each), then the warp walks the words with candidates
+  for (int64_t w0 = v.wlo + gw * 32; w0 < v.whi; w0 += nw * 32) {
+    const int64_t wk = w0 + lane;
+    const uint32_t vis_k = wk < v.whi ? v.visited[wk] : 0xFFFFFFFFu;
+    const uint32_t cand_k = wk < v.whi ? owned_mask(wk, v.lo, v.hi) & ~vis_k & v.nonisol[wk] : 0u;
+    for (unsigned todo = __ballot_sync(0xffffffffu, cand_k != 0); todo; todo &= todo - 1) {
+      const int jw = __ffs(todo) - 1;
+      const int64_t w = w0 + jw;
+      const uint32_t vis = __shfl_sync(0xffffffffu, vis_k, jw);
+      const uint32_t cand = __shfl_sync(0xffffffffu, cand_k, jw);
+      const int64_t u = (w << 5) + lane;
+      bool found = false;
+      uint32_t par = 0;
+      const bool is_cand = (cand >> lane) & 1u;
+      int64_t b = 0, e = 0;
+      if (is_cand) {
+        // the lowest-id neighbour (a hub, on Kronecker graphs) decides most
+        // candidates: read it from the per-vertex table (coalesced across the
+        // warp); the row bounds are fetched alongside, not after it
+        const uint32_t f = __ldg(v.first_nbr + u);
+        b = __ldg(v.off + u) + 1;
+        e = __ldg(v.off + u + 1);
+        ++ex;
+        if ((front[f >> 5] >> (f & 31)) & 1u) {
+          found = true;
+          par = f;
+        }
       }
-    }
-    if (is_cand && !found) {
-      for (int64_t j = b; j < e && !found; j += kBuBatch) {
-        uint32_t p[kBuBatch];
-        bool hit[kBuBatch];
-#pragma unroll
-        for (int k = 0; k < kBuBatch; ++k) p[k] = j + k < e ? ld_stream_u32(adj + j + k) : 0u;
-#pragma unroll
-        for (int k = 0; k < kBuBatch; ++k)
-          hit[k] = j + k < e && ((front[p[k] >> 5] >> (p[k] & 31)) & 1u);
-#pragma unroll
-        for (int k = 0; k < kBuBatch; ++k) {
-          if (!found && j + k < e) {
-            ++ex;
-            if (hit[k]) {
-              found = true;
-              par = p[k];
+      if (is_cand && !found) {
+        for (int64_t j = b; j < e && !found; j += kBuBatch) {
+          uint32_t p[kBuBatch];
+          bool hit[kBuBatch];
+  #pragma unroll
+          for (int k = 0; k < kBuBatch; ++k) p[k] = j + k < e ? ld_stream_u32(adj + j + k) : 0u;
+  #pragma unroll
+          for (int k = 0; k < kBuBatch; ++k)
+            hit[k] = j + k < e && ((front[p[k] >> 5] >> (p[k] & 31)) & 1u);
+  #pragma unroll
+          for (int k = 0; k < kBuBatch; ++k) {
+            if (!found && j + k < e) {
+              ++ex;
+              if (hit[k]) {
+                found = true;
+                par = p[k];
+              }
             }
           }
         }
       }
+      const uint32_t nbits = __ballot_sync(0xffffffffu, found);
+      if (lane == 0 && nbits) v.visited[w] = vis | nbits;  // this node is the word's only writer
+      if (kParents && found) v.parent[u] = par;
     }
-    const uint32_t nbits = __ballot_sync(0xffffffffu, found);
-    if (lane == 0 && nbits) v.visited[w] = vis | nbits;  // this node is the word's only writer
-    if (kParents && found) v.parent[u] = par;
   }
   ex = (unsigned long long)warp_sum_i64((int64_t)ex);
   if (lane == 0 && ex) atomicAdd(examined, ex);
@@ -1394,7 +1405,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       if (part_timing) BFB_CUDA(cudaEventRecord(D->part_ev[g], s));
       PartView v = view_of(ctx, ctx->parts[g]);
       if (bottom_up) {
-        const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo) * 32, 256, sms, 8);
+        const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
         unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
         if (ctx->want_parents)
           k_bottom_up<true><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
@@ -2126,7 +2137,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     PartView v = view_of(ctx, p);
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
     if (bottom_up) {
-      const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo) * 32, 256, sms, 8);
+      const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
       unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
       if (ctx->want_parents)
         k_bottom_up<true><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
