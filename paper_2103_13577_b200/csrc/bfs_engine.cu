@@ -895,6 +895,69 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
 // them into bit slices of the level index, then lanes take 4 vertices each
 // (shuffles) and write d_local with 16-byte stores, 512 contiguous bytes per
 // warp store.
+// Bit slices of one unit (32 words): lane k folds word k of every level
+// bitmap into five words holding bit k of the level index for each of the
+// word's 32 vertices, plus "in some bitmap" and the visited word.
+struct LevelSlices {
+  uint32_t s[5], any, vis;
+};
+
+__device__ __forceinline__ void load_level_slices(const uint32_t* __restrict__ lvbits, int64_t pad,
+                                                  int nl, const uint32_t* __restrict__ visited,
+                                                  int64_t wk, bool in, LevelSlices& L) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) L.s[k] = 0u;
+  L.any = 0u;
+#pragma unroll
+  for (int l = 1; l < kLevelBits; ++l) {
+    const uint32_t x = (l <= nl && in) ? __ldg(lvbits + l * pad + wk) : 0u;
+    L.any |= x;
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+      if ((l >> k) & 1) L.s[k] |= x;
+  }
+  L.vis = in ? __ldg(visited + wk) : 0u;
+}
+
+// d_local of one unit from its slices: 8 passes of 128 vertices, lane = 4
+// consecutive vertices of word q * 4 + lane / 8, one 16-byte store each (a
+// warp writes 512 contiguous bytes per pass).
+__device__ __forceinline__ void store_unit_levels(const LevelSlices& L, int64_t w0,
+                                                  uint32_t* __restrict__ level, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 3, b0 = (lane & 7) * 4;
+#pragma unroll 2
+  for (int q = 0; q < 8; ++q) {
+    const int j = q * 4 + sub;
+    uint32_t sl[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) sl[k] = __shfl_sync(0xffffffffu, L.s[k], j) >> b0;
+    const uint32_t aj = __shfl_sync(0xffffffffu, L.any, j) >> b0;
+    const uint32_t vj = __shfl_sync(0xffffffffu, L.vis, j) >> b0;
+    const int64_t u0 = ((w0 + j) << 5) + b0;
+    if (u0 >= n) continue;
+    uint32_t lv[4];
+    bool keep = false;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      uint32_t l = 0;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) l |= ((sl[k] >> t) & 1u) << k;
+      const bool found = (aj >> t) & 1u, seen = (vj >> t) & 1u;
+      lv[t] = found ? l : kNone;
+      keep |= !found && seen;
+    }
+    if (u0 + 4 <= n && !keep) {
+      *reinterpret_cast<uint4*>(level + u0) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+    } else {
+      for (int t = 0; t < 4 && u0 + t < n; ++t)
+        if (((aj >> t) & 1u) || !((vj >> t) & 1u)) level[u0 + t] = lv[t];
+    }
+  }
+}
+
+// Units are taken two at a time so each warp has both units' bitmap loads in
+// flight before the stores.
 __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __restrict__ lvbits,
                                                           int64_t pad, int nl,
                                                           const uint32_t* __restrict__ visited,
@@ -902,56 +965,16 @@ __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __rest
   const int lane = threadIdx.x & 31;
   const int64_t nwords = (n + 31) / 32;
   const int64_t nunits = (nwords + 31) / 32;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t unit = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; unit < nunits;
-       unit += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t w0 = unit * 32;
-    const int64_t wk = w0 + lane;
-    const bool in = wk < nwords;
-    // The level bitmaps are disjoint, so a vertex's level l is the OR of the
-    // bitmaps' indices: bit-slice it into five words (bit k of l for each of
-    // this word's 32 vertices) plus "in some bitmap".
-    uint32_t slice[5] = {0u, 0u, 0u, 0u, 0u}, any = 0u;
-#pragma unroll
-    for (int l = 1; l < kLevelBits; ++l) {
-      const uint32_t x = (l <= nl && in) ? __ldg(lvbits + l * pad + wk) : 0u;
-      any |= x;
-#pragma unroll
-      for (int k = 0; k < 5; ++k)
-        if ((l >> k) & 1) slice[k] |= x;
-    }
-    const uint32_t vis = in ? __ldg(visited + wk) : 0u;
-    // 8 passes of 128 vertices: lane = 4 consecutive vertices of word
-    // q * 4 + lane / 8, one 16-byte store each (a warp writes 512 contiguous
-    // bytes per pass)
-    const int sub = lane >> 3, b0 = (lane & 7) * 4;
-#pragma unroll 2
-    for (int q = 0; q < 8; ++q) {
-      const int j = q * 4 + sub;
-      uint32_t sl[5];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) sl[k] = __shfl_sync(0xffffffffu, slice[k], j) >> b0;
-      const uint32_t aj = __shfl_sync(0xffffffffu, any, j) >> b0;
-      const uint32_t vj = __shfl_sync(0xffffffffu, vis, j) >> b0;
-      const int64_t u0 = ((w0 + j) << 5) + b0;
-      if (u0 >= n) continue;
-      uint32_t lv[4];
-      bool keep = false;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        uint32_t l = 0;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) l |= ((sl[k] >> t) & 1u) << k;
-        const bool found = (aj >> t) & 1u, seen = (vj >> t) & 1u;
-        lv[t] = found ? l : kNone;
-        keep |= !found && seen;
-      }
-      if (u0 + 4 <= n && !keep) {
-        *reinterpret_cast<uint4*>(level + u0) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
-      } else {
-        for (int t = 0; t < 4 && u0 + t < n; ++t)
-          if (((aj >> t) & 1u) || !((vj >> t) & 1u)) level[u0 + t] = lv[t];
-      }
-    }
+       unit += 2 * nw) {
+    const int64_t unit2 = unit + nw;
+    LevelSlices A, B;
+    load_level_slices(lvbits, pad, nl, visited, unit * 32 + lane, unit * 32 + lane < nwords, A);
+    load_level_slices(lvbits, pad, nl, visited, unit2 * 32 + lane,
+                      unit2 < nunits && unit2 * 32 + lane < nwords, B);
+    store_unit_levels(A, unit * 32, level, n);
+    if (unit2 < nunits) store_unit_levels(B, unit2 * 32, level, n);
   }
 }
 
