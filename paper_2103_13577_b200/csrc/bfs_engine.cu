@@ -908,13 +908,14 @@ __device__ __forceinline__ void load_level_slices(const uint32_t* __restrict__ l
 #pragma unroll
   for (int k = 0; k < 5; ++k) L.s[k] = 0u;
   L.any = 0u;
+  if (in) {
+#pragma unroll 4
+    for (int l = 1; l <= nl; ++l) {
+      const uint32_t x = __ldg(lvbits + l * pad + wk);
+      L.any |= x;
 #pragma unroll
-  for (int l = 1; l < kLevelBits; ++l) {
-    const uint32_t x = (l <= nl && in) ? __ldg(lvbits + l * pad + wk) : 0u;
-    L.any |= x;
-#pragma unroll
-    for (int k = 0; k < 5; ++k)
-      if ((l >> k) & 1) L.s[k] |= x;
+      for (int k = 0; k < 5; ++k) L.s[k] |= x & (0u - (uint32_t)((l >> k) & 1));
+    }
   }
   L.vis = in ? __ldg(visited + wk) : 0u;
 }
