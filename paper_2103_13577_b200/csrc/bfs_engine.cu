@@ -861,12 +861,12 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
         for (int64_t j = b; j < e && !found; j += kBuBatch) {
           uint32_t p[kBuBatch];
           bool hit[kBuBatch];
-  #pragma unroll
+#pragma unroll
           for (int k = 0; k < kBuBatch; ++k) p[k] = j + k < e ? ld_stream_u32(adj + j + k) : 0u;
-  #pragma unroll
+#pragma unroll
           for (int k = 0; k < kBuBatch; ++k)
             hit[k] = j + k < e && ((front[p[k] >> 5] >> (p[k] & 31)) & 1u);
-  #pragma unroll
+#pragma unroll
           for (int k = 0; k < kBuBatch; ++k) {
             if (!found && j + k < e) {
               ++ex;
