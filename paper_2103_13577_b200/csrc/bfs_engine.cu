@@ -427,13 +427,12 @@ __device__ __forceinline__ uint32_t owned_mask(int64_t w, int64_t lo, int64_t hi
 }
 
 // Commit of the owned words, in warp units of 32 words (1024 vertices):
-//   k_commit_count  per unit: owned new vertices and their degree sum
+//   k_commit_count  per unit: owned new vertices and their degree sum (from
+//                   the 16-bit degree table), the level's new-vertex bitmap
 //   k_unit_scan_*   device-wide exclusive scan of the (count, degree) pairs
-//   k_commit_write  per unit, from its prefix: levels, q_v, q_pre, tile
+//   k_commit_write  per unit, from its prefix: q_v, q_pre, q_base, tile
 //                   starts, start snapshot -- q_local in ascending order
-// Thread = word: each lane walks the set bits of its own word (independent
-// offsets loads, high MLP, no block barriers); one warp scan per unit turns
-// per-word (count, degree) into positions.
+// Lane = word for the bitmaps; no block barriers.
 __device__ __forceinline__ void unit_word(const PartView& v, int64_t unit, int lane, uint32_t& a,
                                           uint32_t& nb, uint32_t& own) {
   const int64_t w = v.abase + unit * 32 + lane;
@@ -615,7 +614,8 @@ __device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vs
 }
 
 // Write pass, per 32-word unit (1024 vertices) and warp:
-//   1. levels of every new vertex (lane = bit, one coalesced store per word);
+//   1. levels >= kLevelBits only (shallower ones come from the level
+//      bitmaps at termination): lane = bit, one coalesced store per word;
 //   2. the owned new vertices compacted into a per-warp shared list in
 //      ascending order (lane = word: position = prefix of the words' counts);
 //   3. the list, 32 vertices at a time, lane = vertex: offsets pair, a warp
@@ -770,9 +770,10 @@ __global__ void __launch_bounds__(256) k_commit_light(PartView v, uint32_t next_
 }
 
 // Commit of the words outside this node's owned range (its replicated
-// d_local): levels of the new vertices, start := visited, the
-// frontier bitmap and the frontier count.  Warp = 32 consecutive words
-// (lane = word for the bitmaps, lane = bit for the coalesced level stores).
+// d_local): the level's new-vertex bitmap (or, past kLevelBits,
+// the levels themselves), start := visited, the frontier bitmap and the
+// frontier count.  Warp = 32 consecutive words (lane = word for the bitmaps,
+// lane = bit for coalesced level stores).
 __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_level) {
   const int lane = threadIdx.x & 31;
   const int64_t span = v.nwords - (v.whi - v.wlo);  // words outside [wlo, whi)

@@ -10,7 +10,7 @@ import sys, os
 sys.path.insert(0, %r)
 from paper_2103_13577_b200 import graphs
 scale = int(os.environ.get("SW_SCALE", "29"))
-g = graphs.kronecker(scale, 8, 1)
+g = graphs.kronecker(scale, int(os.environ.get("SW_EF", "8")), 1)
 dg = g.device
 roots = graphs.sample_roots(g, 6)
 for parents, direction in ((False, "top-down"), (True, "top-down"), (True, "optimizing"), (False, "optimizing")):
