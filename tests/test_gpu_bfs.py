@@ -298,3 +298,24 @@ def test_deep_graph_levels_past_the_level_bitmaps(cn):
             assert np.array_equal(d.d, ref), (cn, direction, root)
             assert not ov.check_parents(off, adj, root, d.d, d.parents)
             assert st.per_level_frontier_size == ob.level_sizes(ref)
+
+
+@pytest.mark.parametrize("direction", ["top-down", "optimizing"])
+def test_tiny_and_ragged_graphs(direction):
+    """Edge cases of the bitmap/word layout: a single vertex, one edge, a
+    vertex count that is not a multiple of 32 (star centred on the last
+    vertex, padded words), and 32 isolated vertices plus one edge at the end."""
+    cases = [(1, []), (2, [(0, 1)]), (33, [(32, i) for i in range(32)]),
+             (65, [(63, 64)]), (1025, [(i, i + 1) for i in range(1000, 1024)])]
+    for n, edges in cases:
+        off, adj = util.csr_of_undirected(n, edges)
+        g = _g(off, adj)
+        for cn in sorted({1, min(2, n), min(3, n)}):
+            p = graphs.partition_1d(g, cn)
+            for root in sorted({0, n - 1, n // 2}):
+                cfg = engine.EngineConfig(fanout=1, parents=True, direction=direction)
+                d, st = engine.run(g, p, root, cfg)
+                ref = ob.bfs_top_down(off, adj, root)
+                assert np.array_equal(d.d, ref), (n, cn, root)
+                assert not ov.check_parents(off, adj, root, d.d, d.parents)
+                assert st.per_level_frontier_size == ob.level_sizes(ref)
