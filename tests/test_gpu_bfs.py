@@ -319,3 +319,27 @@ def test_tiny_and_ragged_graphs(direction):
                 assert np.array_equal(d.d, ref), (n, cn, root)
                 assert not ov.check_parents(off, adj, root, d.d, d.parents)
                 assert st.per_level_frontier_size == ob.level_sizes(ref)
+
+
+@pytest.mark.slow
+def test_config5_s29_ef8_headline_properties():
+    """BASELINE config 5 (the headline graph, Kronecker s29 ef8) at full size on
+    one GPU: for three Graph500 roots the device certificate (SPEC.md:130-132 +
+    parent validity) holds for top-down and direction-optimizing runs, both
+    give identical levels (sha) and frontier sizes, and the sizes add up to
+    the reached count."""
+    g = graphs.kronecker(29, 8, 1)
+    dg = g.device
+    assert g.num_vertices == 1 << 29 and dg.max_degree > 0
+    dg.setup(dg.partition_1d(1), 1, "butterfly", parents=True)
+    for r in graphs.sample_roots(g, 3):
+        out = {}
+        for direction in ("top-down", "optimizing"):
+            dg.set_direction(direction)
+            lv, _, sizes, st, _ = dg.bfs(int(r))
+            assert dg.validate(int(r)) == 0, direction
+            assert sum(sizes) == st.reached == int((lv != U).sum())
+            out[direction] = (sha16(lv), tuple(sizes), st.traversed_edges)
+            del lv
+        assert out["top-down"] == out["optimizing"], int(r)
+    dg.set_direction("top-down")
