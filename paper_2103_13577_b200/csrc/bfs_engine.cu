@@ -271,6 +271,41 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
   return next;
 }
 
+// A tile lying inside one row (hub rows: most of the edges of the hub-heavy
+// early levels): no row resolution, no per-batch q loads, and each lane keeps
+// kRunItems probes in flight.
+constexpr int kRunItems = 12;  // measured at s29 (parents on): 8 -> 218.7, 12 -> 219.1, 16 -> 217.7 GTEP/s
+
+template <bool kParents>
+__device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t* __restrict__ adj,
+                                               int64_t e0, int span, uint32_t row, uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  const int64_t base = __ldg(v.q_base + row) + e0;
+  const uint32_t src = kParents ? __ldg(v.q_v + row) : 0u;
+  uint32_t* __restrict__ visited = v.visited;
+  for (int k = 0; k < span; k += 32 * kRunItems) {
+    uint32_t u[kRunItems], wv[kRunItems];
+#pragma unroll
+    for (int it = 0; it < kRunItems; ++it) {
+      const int r = k + it * 32 + lane;
+      u[it] = r < span ? adj_word(adj + base + r, pol) : 0u;
+    }
+#pragma unroll
+    for (int it = 0; it < kRunItems; ++it) {
+      const int r = k + it * 32 + lane;
+      wv[it] = r < span ? visited[u[it] >> 5] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int it = 0; it < kRunItems; ++it) {
+      const uint32_t bit = 1u << (u[it] & 31);
+      if (!(wv[it] & bit)) {
+        atomicOr(&visited[u[it] >> 5], bit);
+        if (kParents) v.parent[u[it]] = src;
+      }
+    }
+  }
+}
+
 // Row of q_local rows [lo, hi] holding edge position `pos` (the last row whose
 // degree prefix is <= pos): 32-ary warp search, 3 steps for a 2048-edge tile.
 __device__ __forceinline__ uint32_t find_row(const int64_t* __restrict__ q_pre, uint32_t lo,
@@ -309,6 +344,10 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const int span = (int)min(kTile, T - e0);
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       uint32_t cur = v.tile_vstart[t];
+      if (cur == ve) {  // the whole tile inside one row
+        expand_row_run<kParents>(v, adj, e0, span, cur, pol);
+        continue;
+      }
       for (int k = 0; k * kSub < span; ++k)
         cur = expand_subtile<kParents>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
                                        cur, ve, le_mask, pol);
