@@ -670,7 +670,6 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
   uint16_t* list = s_list[threadIdx.x >> 5];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const unsigned lt = (1u << lane) - 1u;
   for (int64_t unit = gw; unit < v.nunits; unit += nw) {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
