@@ -139,7 +139,7 @@ struct DevGraph {
   DevBuf<uint32_t> adj;      // m
   DevBuf<uint32_t> nonisol;  // bitmap of degree > 0 (bottom-up candidates), built at engine setup
   DevBuf<uint16_t> deg16;    // min(degree, 65535) per vertex (commit degree sums), engine setup
-  DevBuf<uint32_t> first_nbr;  // lowest-id neighbour per vertex (bottom-up first probe), engine setup
+  DevBuf<uint2> first_nbr;    // two lowest-id neighbours per vertex (bottom-up first probes), engine setup
   bool valid = false;
 };
 

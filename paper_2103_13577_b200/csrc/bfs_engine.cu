@@ -71,7 +71,7 @@ struct PartView {
   const int64_t* off;  // CSR offsets (rows of q_v)
   const uint32_t* nonisol;  // degree > 0 bitmap
   const uint16_t* deg16;    // min(degree, 65535)
-  const uint32_t* first_nbr;  // lowest-id neighbour
+  const uint2* first_nbr;    // two lowest-id neighbours (kNone if absent)
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
@@ -883,20 +883,28 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
       uint32_t par = 0;
       const bool is_cand = (cand >> lane) & 1u;
       int64_t b = 0, e = 0;
+      bool more = false;
       if (is_cand) {
-        // the lowest-id neighbour (a hub, on Kronecker graphs) decides most
-        // candidates: read it from the per-vertex table (coalesced across the
-        // warp); the row bounds are fetched alongside, not after it
-        const uint32_t f = __ldg(v.first_nbr + u);
-        b = __ldg(v.off + u) + 1;
-        e = __ldg(v.off + u + 1);
+        // the two lowest-id neighbours (hubs, on Kronecker graphs) decide most
+        // candidates -- all of those with degree <= 2 -- from a per-vertex
+        // table read coalesced across the warp; only the rest load the row
+        const uint2 f = __ldg(v.first_nbr + u);
+        more = __ldg(v.deg16 + u) > 2;
         ++ex;
-        if ((front[f >> 5] >> (f & 31)) & 1u) {
+        if ((front[f.x >> 5] >> (f.x & 31)) & 1u) {
           found = true;
-          par = f;
+          par = f.x;
+        } else if (f.y != kNone) {
+          ++ex;
+          if ((front[f.y >> 5] >> (f.y & 31)) & 1u) {
+            found = true;
+            par = f.y;
+          }
         }
       }
-      if (is_cand && !found) {
+      if (is_cand && !found && more) {
+        b = __ldg(v.off + u) + 2;
+        e = __ldg(v.off + u + 1);
         for (int64_t j = b; j < e && !found; j += kBuBatch) {
           uint32_t p[kBuBatch];
           bool hit[kBuBatch];
@@ -1032,7 +1040,7 @@ __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n
 // Per-vertex tables built once per engine setup (lane = vertex): the bitmap
 // of degree > 0 and min(degree, 65535) as 16 bits.
 __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                int64_t n, uint32_t* nonisol, uint16_t* deg16, uint32_t* first_nbr,
+                                int64_t n, uint32_t* nonisol, uint16_t* deg16, uint2* first_nbr,
                                 int64_t nwords_pad) {
   const int lane = threadIdx.x & 31;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords_pad;
@@ -1043,7 +1051,7 @@ __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t*
     const unsigned b = __ballot_sync(0xffffffffu, d > 0);
     if (lane == 0) nonisol[w] = b;
     deg16[u] = (uint16_t)min(d, (int64_t)0xFFFF);
-    first_nbr[u] = d > 0 ? __ldg(adj + o) : kNone;
+    first_nbr[u] = make_uint2(d > 0 ? __ldg(adj + o) : kNone, d > 1 ? __ldg(adj + o + 1) : kNone);
   }
 }
 
