@@ -191,6 +191,25 @@ struct Part {
 
 namespace bfb {
 struct EngineTables;  // bfs_engine.cu: device-side pointer/schedule tables
+
+// Result read-out (host_out.cu): a page-locked staging area for the packed
+// D2H copy and one event per pipelined chunk.
+struct HostStage {
+  void* p = nullptr;
+  size_t bytes = 0;
+  std::vector<cudaEvent_t> ev;
+  HostStage() = default;
+  HostStage(const HostStage&) = delete;
+  HostStage& operator=(const HostStage&) = delete;
+  ~HostStage() { release(); }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+  }
+};
 }
 
 struct bfb_ctx {
@@ -222,6 +241,9 @@ struct bfb_ctx {
   // text ingestion: edges parsed by bfb_parse_text, awaiting the CSR build
   bfb::DevBuf<uint2> parsed;
   int64_t parsed_m = 0;
+  // result read-out: packed levels on device, staging in host memory
+  bfb::DevBuf<uint32_t> packed;
+  bfb::HostStage stage;
 };
 
 namespace bfb {
@@ -246,6 +268,11 @@ int graph_load(bfb_ctx* ctx, const char* path);
 int copy_edges(bfb_ctx* ctx, uint32_t* out);
 int partition_1d(bfb_ctx* ctx, int parts, int64_t* out);
 int count_nonisolated(bfb_ctx* ctx, int64_t* out);
+// host_out.cu: levels / parents from device to host (packed, pipelined,
+// unpacked by host threads)
+int read_levels(bfb_ctx* ctx, const uint32_t* level, int64_t n, int64_t num_levels,
+                uint32_t* out, cudaStream_t s);
+int read_parents(bfb_ctx* ctx, const uint32_t* parent, int64_t n, int64_t* out, cudaStream_t s);
 int select_nonisolated(bfb_ctx* ctx, const int64_t* ranks, int64_t k, int64_t* out);
 
 // scan.cu: exclusive scan of n values produced by a loader -> int64 out[0..n]

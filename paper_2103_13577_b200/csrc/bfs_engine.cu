@@ -1632,9 +1632,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   std::vector<int64_t> hw(P);
   BFB_CUDA(cudaMemcpyAsync(hw.data(), ctx->high_water.p, P * sizeof(int64_t),
                            cudaMemcpyDeviceToHost, s));
-  if (levels_out)
-    BFB_CUDA(cudaMemcpyAsync(levels_out, ctx->parts[0].level.p, n * sizeof(uint32_t),
-                             cudaMemcpyDeviceToHost, s));
+  if (levels_out) BFB_TRY(read_levels(ctx, ctx->parts[0].level.p, n, nsizes, levels_out, s));
   BFB_CUDA(cudaStreamSynchronize(s));
   float elapsed = 0;
   BFB_CUDA(cudaEventElapsedTime(&elapsed, D->ev[0], D->ev[1]));
@@ -1643,10 +1641,8 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     if (P == 1)
       k_mask_parents<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(ctx->parts[0].level.p,
                                                               ctx->parts[0].parent.p, n);
-    std::vector<uint32_t> tmp(n);
-    BFB_CUDA(cudaMemcpyAsync(tmp.data(), parents_dev, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    BFB_TRY(read_parents(ctx, parents_dev, n, parents_out, s));
     BFB_CUDA(cudaStreamSynchronize(s));
-    for (int64_t i = 0; i < n; ++i) parents_out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
   }
   if (hw_out) std::memcpy(hw_out, hw.data(), P * sizeof(int64_t));
   ctx->have_run = true;
@@ -1683,8 +1679,8 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
 
 int engine_copy_levels(bfb_ctx* ctx, uint32_t* out) {
   if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
-  BFB_CUDA(cudaMemcpy(out, ctx->parts[0].level.p, ctx->g.n * sizeof(uint32_t),
-                      cudaMemcpyDeviceToHost));
+  BFB_TRY(read_levels(ctx, ctx->parts[0].level.p, ctx->g.n, ctx->last_levels, out, ctx->stream));
+  BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   return BFB_OK;
 }
 
@@ -1708,9 +1704,8 @@ int engine_copy_parents(bfb_ctx* ctx, int64_t* out) {
   if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
   const uint32_t* src = nullptr;
   BFB_TRY(output_parents(ctx, &src));
-  std::vector<uint32_t> tmp(ctx->g.n);
-  BFB_CUDA(cudaMemcpy(tmp.data(), src, ctx->g.n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  for (int64_t i = 0; i < ctx->g.n; ++i) out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
+  BFB_TRY(read_parents(ctx, src, ctx->g.n, out, ctx->stream));
+  BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   return BFB_OK;
 }
 
@@ -1958,6 +1953,7 @@ int rank_finish(bfb_ctx* ctx, bfb_run_stats* st) {
   float elapsed = 0;
   BFB_CUDA(cudaEventElapsedTime(&elapsed, D->ev[0], D->ev[1]));
   ctx->have_run = true;
+  ctx->last_levels = D->levels;
   if (st) {
     std::memset(st, 0, sizeof(*st));
     st->levels = D->levels;
@@ -1990,11 +1986,8 @@ int rank_parents(bfb_ctx* ctx, int64_t* out) {
   const int64_t n = ctx->g.n;
   k_parents_min<<<grid_cap(n, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
       D->parents.p, P, n, D->parents_final.p);
-  std::vector<uint32_t> tmp(n);
-  BFB_CUDA(cudaMemcpyAsync(tmp.data(), D->parents_final.p, n * sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost, ctx->stream));
+  BFB_TRY(read_parents(ctx, D->parents_final.p, n, out, ctx->stream));
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (int64_t i = 0; i < n; ++i) out[i] = tmp[i] == kNone ? -1 : (int64_t)tmp[i];
   return BFB_OK;
 }
 
