@@ -52,6 +52,17 @@ class _PinnedPool:
 _POOL = _PinnedPool()
 
 
+def levels_readout_bytes(num_vertices, num_levels):
+    """Bytes the levels read-out moves device -> host for a run with
+    num_levels levels (csrc/host_out.cu read_levels): 4 bits per vertex up to
+    15 levels, 8 bits up to 255, else 32."""
+    if num_levels <= 15:
+        return (num_vertices + 1) // 2
+    if num_levels <= 255:
+        return num_vertices
+    return 4 * num_vertices
+
+
 class DeviceGraph:
     """CSR graph resident on one GPU plus its ButterFly BFS engine state."""
 
