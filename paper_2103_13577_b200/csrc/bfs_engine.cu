@@ -662,9 +662,17 @@ __device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vs
 //      q_v / q_pre / q_base stores; tile starts for the tiles whose first edge
 //      falls in the vertex's row.
 // A 32-vertex degree sum fits 32 bits when max degree < 2^26 (kWide = false).
-template <bool kWide>
+//
+// Two builds are launched back to back and the level's new-vertex count
+// (ctr->q_count, from the scan) picks the one that runs: kPrefetch (dense
+// levels, >= pf_min new vertices) loads the next batch's offsets before the
+// current batch's scan and stores, two batches of gathers in flight per warp
+// at 44 registers; the plain build keeps 38 registers and one more CTA per SM
+// for the sparse levels, which are bound by the per-unit bitmap loads.
+template <bool kWide, bool kPrefetch>
 __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
-                                                      uint32_t next_level) {
+                                                      uint32_t next_level, int64_t pf_min) {
+  if ((v.ctr->q_count >= pf_min) != kPrefetch) return;
   __shared__ uint16_t s_list[256 / 32][1024];  // unit-local vertex index (word * 32 + bit)
   const int lane = threadIdx.x & 31;
   uint16_t* list = s_list[threadIdx.x >> 5];
@@ -695,12 +703,33 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
     __syncwarp();
     const int64_t p0 = v.upos[unit];
     int64_t ecarry = v.uepre[unit];
+    uint32_t un = 0;
+    int64_t o0n = 0, o1n = 0;
+    if (kPrefetch) {
+      un = lane < total ? (uint32_t)((w0 << 5) + list[lane]) : 0u;
+      o0n = lane < total ? __ldg(off + un) : 0;
+      o1n = lane < total ? __ldg(off + un + 1) : 0;
+    }
     for (int i = 0; i < total; i += 32) {
       const int k = i + lane;
       const bool ok = k < total;
-      const uint32_t u = ok ? (uint32_t)((w0 << 5) + list[k]) : 0u;
-      const int64_t o0 = ok ? __ldg(off + u) : 0;
-      const int64_t d = ok ? __ldg(off + u + 1) - o0 : 0;
+      uint32_t u;
+      int64_t o0, d;
+      if (kPrefetch) {
+        u = un;
+        o0 = o0n;
+        d = o1n - o0n;
+        if (i + 32 < total) {
+          const bool okn = k + 32 < total;
+          un = okn ? (uint32_t)((w0 << 5) + list[k + 32]) : 0u;
+          o0n = okn ? __ldg(off + un) : 0;
+          o1n = okn ? __ldg(off + un + 1) : 0;
+        }
+      } else {
+        u = ok ? (uint32_t)((w0 << 5) + list[k]) : 0u;
+        o0 = ok ? __ldg(off + u) : 0;
+        d = ok ? __ldg(off + u + 1) - o0 : 0;
+      }
       int64_t inc;
       if (kWide) {
         inc = warp_inclusive_i64(d);
@@ -1202,13 +1231,19 @@ int launch_commit_write(const PartView& v, const int64_t* off, uint32_t next_lev
     return 1;
   }
   k_unit_scan_apply<<<(unsigned)ntiles, 256, 0, s>>>(v);
-  if (v.wide)
-    k_commit_write<true><<<resident_grid(k_commit_write<true>, work, 256, sms), 256, 0, s>>>(
-        v, off, next_level);
-  else
-    k_commit_write<false><<<resident_grid(k_commit_write<false>, work, 256, sms), 256, 0, s>>>(
-        v, off, next_level);
-  return 2;
+  const int64_t pf_min = v.nunits * 16;  // 1/64 of the part's vertices
+  if (v.wide) {
+    k_commit_write<true, false><<<resident_grid(k_commit_write<true, false>, work, 256, sms), 256,
+                                   0, s>>>(v, off, next_level, pf_min);
+    k_commit_write<true, true><<<resident_grid(k_commit_write<true, true>, work, 256, sms), 256,
+                                  0, s>>>(v, off, next_level, pf_min);
+  } else {
+    k_commit_write<false, false><<<resident_grid(k_commit_write<false, false>, work, 256, sms),
+                                   256, 0, s>>>(v, off, next_level, pf_min);
+    k_commit_write<false, true><<<resident_grid(k_commit_write<false, true>, work, 256, sms), 256,
+                                  0, s>>>(v, off, next_level, pf_min);
+  }
+  return 3;
 }
 
 // Bottom-up level commit (one pass); rebuild: the queue for a following

@@ -19,6 +19,7 @@ ap.add_argument("--edge-factor", type=int, default=8)
 ap.add_argument("--parents", type=int, default=1)
 ap.add_argument("--direction", default="top-down")
 ap.add_argument("--runs", type=int, default=1)
+ap.add_argument("--levels", type=int, default=0, help="read the levels out after the last run")
 a = ap.parse_args()
 g = graphs.kronecker(a.scale, a.edge_factor, 1)
 dg = g.device
@@ -26,8 +27,8 @@ root = int(graphs.sample_roots(g, 1)[0])
 dg.setup(dg.partition_1d(1), 1, "butterfly", parents=bool(a.parents))
 dg.set_direction(a.direction)
 dg.set_timing(True)
-for _ in range(1 + a.runs):
-    _, _, sizes, st, _ = dg.bfs(root, levels=False)
+for i in range(1 + a.runs):
+    _, _, sizes, st, _ = dg.bfs(root, levels=bool(a.levels) and i == a.runs)
     print(f"root {root} levels {len(sizes)} sizes {sizes} ms {st.elapsed_ms:.2f} "
           f"expand {st.expand_ms:.2f} commit {st.commit_ms:.2f} edges {st.traversed_edges}",
           flush=True)
