@@ -199,6 +199,14 @@ __device__ __forceinline__ uint32_t adj_word(const uint32_t* p, uint64_t pol) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t probe_word(const uint32_t* p) {
+#ifdef BFB_PROBE_NC
+  return __ldg(p);
+#else
+  return *p;
+#endif
+}
+
 // One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
 // with rb the row holding edge r0 and ve the last row that can matter.
 // Returns the row holding edge r0 + kSub (the next subtile's cursor).
@@ -256,7 +264,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
   uint32_t wv[kExpandItems];
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it)
-    wv[it] = ((done >> it) & 1u) ? visited[u[it] >> 5] : 0xFFFFFFFFu;
+    wv[it] = ((done >> it) & 1u) ? probe_word(visited + (u[it] >> 5)) : 0xFFFFFFFFu;
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
     const uint32_t bit = 1u << (u[it] & 31);
@@ -293,7 +301,7 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
       const int r = k + it * 32 + lane;
-      wv[it] = r < span ? visited[u[it] >> 5] : 0xFFFFFFFFu;
+      wv[it] = r < span ? probe_word(visited + (u[it] >> 5)) : 0xFFFFFFFFu;
     }
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {

@@ -7,6 +7,7 @@
 // k_expand_w) over a buffer of the bitmap's size, so probes/s here is the
 // ceiling bench.py reports the expand kernel against (roofline "l2_probe").
 #include <algorithm>
+#include <cstdlib>
 
 #include "bfb_internal.cuh"
 
@@ -15,8 +16,12 @@ namespace {
 
 constexpr int kProbeItems = 8;
 
-__global__ void __launch_bounds__(256) k_probe_peak(const uint32_t* __restrict__ buf,
-                                                    uint32_t nwords, int steps,
+// kNC: the loads go through the non-coherent path (ld.global.nc, what a
+// const __restrict__ pointer compiles to); the expand's probes are plain
+// ld.global (the bitmap is written during the kernel), so the ceiling is
+// measured with kNC = false.
+template <bool kNC>
+__global__ void __launch_bounds__(256) k_probe_peak(const uint32_t* buf, uint32_t nwords, int steps,
                                                     uint32_t* __restrict__ sink) {
   uint64_t x = 0x9E3779B97F4A7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1);
   uint32_t acc = 0;
@@ -27,7 +32,12 @@ __global__ void __launch_bounds__(256) k_probe_peak(const uint32_t* __restrict__
       x ^= x << 13;
       x ^= x >> 7;
       x ^= x << 17;
-      w[k] = buf[__umulhi((uint32_t)(x >> 32), nwords)];  // uniform in [0, nwords)
+      const uint32_t* p = buf + __umulhi((uint32_t)(x >> 32), nwords);  // uniform in [0, nwords)
+      if (kNC) {
+        w[k] = __ldg(p);
+      } else {
+        asm volatile("ld.global.u32 %0, [%1];" : "=r"(w[k]) : "l"(p));
+      }
     }
 #pragma unroll
     for (int k = 0; k < kProbeItems; ++k) acc ^= w[k];
@@ -51,13 +61,15 @@ int probe_peak(bfb_ctx* ctx, int64_t bytes, int64_t* probes_out, double* ms_out)
   cudaStream_t s = ctx->stream;
   k_fill<<<ctx->num_sms * 8, 256, 0, s>>>(buf.p, nwords);
   const int grid = ctx->num_sms * 8, steps = 256;
-  k_probe_peak<<<grid, 256, 0, s>>>(buf.p, nwords, steps, sink.p);  // warm L2
+  const char* nc_env = std::getenv("BFB_PROBE_NC");  // developer switch: the .nc path instead
+  auto kernel = nc_env && nc_env[0] == '1' ? k_probe_peak<true> : k_probe_peak<false>;
+  kernel<<<grid, 256, 0, s>>>(buf.p, nwords, steps, sink.p);  // warm L2
   cudaEvent_t e0, e1;
   BFB_CUDA(cudaEventCreate(&e0));
   BFB_CUDA(cudaEventCreate(&e1));
   BFB_CUDA(cudaEventRecord(e0, s));
   const int reps = 5;
-  for (int r = 0; r < reps; ++r) k_probe_peak<<<grid, 256, 0, s>>>(buf.p, nwords, steps, sink.p);
+  for (int r = 0; r < reps; ++r) kernel<<<grid, 256, 0, s>>>(buf.p, nwords, steps, sink.p);
   BFB_CUDA(cudaEventRecord(e1, s));
   BFB_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
