@@ -993,15 +993,32 @@ __device__ __forceinline__ void load_level_slices(const uint32_t* __restrict__ l
   for (int k = 0; k < 5; ++k) L.s[k] = 0u;
   L.any = 0u;
   if (in) {
-#pragma unroll 4
-    for (int l = 1; l <= nl; ++l) {
+    // fully unrolled: the level's bits are compile-time, one OR per set bit
+#pragma unroll
+    for (int l = 1; l < kLevelBits; ++l) {
+      if (l > nl) break;
       const uint32_t x = __ldg(lvbits + l * pad + wk);
       L.any |= x;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) L.s[k] |= x & (0u - (uint32_t)((l >> k) & 1));
+      for (int k = 0; k < 5; ++k)
+        if ((l >> k) & 1) L.s[k] |= x;
     }
   }
   L.vis = in ? __ldg(visited + wk) : 0u;
+}
+
+// Bits 0..3 of n to bit 0 of bytes 0..3 (the four copies n << 7i do not
+// overlap, so the product has no carries).
+__device__ __forceinline__ uint32_t spread4(uint32_t n) { return (n * 0x00204081u) & 0x01010101u; }
+
+// Byte t of x as a uint32, its top bit replicated into bytes 1..3 (prmt sign
+// mode): 0xFF -> 0xFFFFFFFF (UNREACHED), levels < 128 zero-extended.
+template <int t>
+__device__ __forceinline__ uint32_t byte_sext(uint32_t x) {
+  uint32_t r;
+  constexpr uint32_t sel = t | ((8 | t) << 4) | ((8 | t) << 8) | ((8 | t) << 12);
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "n"(sel));
+  return r;
 }
 
 // d_local of one unit from its slices: 8 passes of 128 vertices, lane = 4
@@ -1021,17 +1038,15 @@ __device__ __forceinline__ void store_unit_levels(const LevelSlices& L, int64_t 
     const uint32_t vj = __shfl_sync(0xffffffffu, L.vis, j) >> b0;
     const int64_t u0 = ((w0 + j) << 5) + b0;
     if (u0 >= n) continue;
-    uint32_t lv[4];
-    bool keep = false;
+    // byte t = level of vertex u0 + t (bit k from slice k), 0xFF if in no bitmap
+    uint32_t bytes = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      uint32_t l = 0;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) l |= ((sl[k] >> t) & 1u) << k;
-      const bool found = (aj >> t) & 1u, seen = (vj >> t) & 1u;
-      lv[t] = found ? l : kNone;
-      keep |= !found && seen;
-    }
+    for (int k = 0; k < 5; ++k) bytes |= spread4(sl[k] & 0xFu) << k;
+    const uint32_t f = aj & 0xFu;
+    bytes |= ~(spread4(f) * 0xFFu);
+    const uint32_t lv[4] = {byte_sext<0>(bytes), byte_sext<1>(bytes), byte_sext<2>(bytes),
+                            byte_sext<3>(bytes)};
+    const bool keep = (vj & ~f & 0xFu) != 0u;  // visited, level in d_local already
     if (u0 + 4 <= n && !keep) {
       *reinterpret_cast<uint4*>(level + u0) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
     } else {
