@@ -72,6 +72,7 @@ struct PartView {
   const uint32_t* nonisol;  // degree > 0 bitmap
   const uint16_t* deg16;    // min(degree, 65535)
   const uint2* first_nbr;    // two lowest-id neighbours (kNone if absent)
+  const uint32_t* adj;       // CSR adjacency (the commit's parent pass)
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
@@ -108,6 +109,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.nonisol = ctx->g.nonisol.p;
   v.deg16 = ctx->g.deg16.p;
   v.first_nbr = ctx->g.first_nbr.p;
+  v.adj = ctx->g.adj.p;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -520,20 +522,31 @@ __device__ __forceinline__ int64_t word_degree_sum16(uint32_t x, int64_t w,
       esc |= db == 0xFFFFu;
     }
   }
-  if (esc) {  // a hub: recount its exact degree
-#pragma unroll 1
-    for (int b = 0; b < 32; ++b) {
-      const uint32_t db = (q[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu;
-      if (((x >> b) & 1u) && db == 0xFFFFu) {
-        const int64_t u = (w << 5) + b;
-        d += (__ldg(off + u + 1) - __ldg(off + u)) - 0xFFFF;
-      }
+  if (esc) {  // a hub: recount its exact degree (re-reading deg16 keeps q in registers)
+    for (uint32_t y = x; y; y &= y - 1) {
+      const int64_t u = (w << 5) + __ffs(y) - 1;
+      if (__ldg(deg16 + u) == 0xFFFFu) d += (__ldg(off + u + 1) - __ldg(off + u)) - 0xFFFF;
     }
   }
   return d;
 }
 
+// Parent pass (kParents; single node, dense levels): phase 1 ran without
+// parent stores, and each owned new vertex u of this level takes as parent
+// its lowest-id neighbour in `start` -- the vertices of levels <= L, all of
+// which are at level L exactly when u is at L + 1 (one at L - 1 or below
+// would have discovered u earlier).  `start` is not written before the write
+// pass, so the probes see exactly levels <= L.  The two lowest neighbours come
+// from the first_nbr table; the row is scanned only when both miss.  One
+// store per reached vertex in ascending order replaces phase 1's random
+// store per clear-probe claim, and the parent is deterministic.
+__device__ __forceinline__ bool in_start(const uint32_t* __restrict__ start, uint32_t z) {
+  return (start[z >> 5] >> (z & 31)) & 1u;
+}
+
+template <bool kParents>
 __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t* __restrict__ off) {
+  __shared__ uint16_t s_list[kParents ? 256 / 32 : 1][kParents ? 1024 : 1];
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -552,6 +565,41 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
     if (lane == 0) {
       v.ucnt[unit] = c;
       v.udeg[unit] = d;
+    }
+    if (kParents && c) {
+      uint16_t* list = s_list[threadIdx.x >> 5];
+      const int cnt = __popc(own);
+      int pos = cnt;
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, pos, k);
+        if (lane >= k) pos += t;
+      }
+      pos -= cnt;
+      for (uint32_t x = own; x; x &= x - 1) list[pos++] = (uint16_t)((lane << 5) + __ffs(x) - 1);
+      __syncwarp();
+      const int64_t ubase = (v.abase + unit * 32) << 5;
+      for (int k = lane; k < (int)c; k += 32) {
+        const uint32_t u = (uint32_t)(ubase + list[k]);
+        const uint2 fn = __ldg(v.first_nbr + u);
+        uint32_t p = kNone;
+        if (fn.x != kNone && in_start(v.start, fn.x)) {
+          p = fn.x;
+        } else if (fn.y != kNone && in_start(v.start, fn.y)) {
+          p = fn.y;
+        } else {
+          const int64_t e = __ldg(off + u + 1);
+          for (int64_t j = __ldg(off + u) + 2; j < e; ++j) {
+            const uint32_t z = __ldg(v.adj + j);
+            if (in_start(v.start, z)) {
+              p = z;
+              break;
+            }
+          }
+        }
+        v.parent[u] = p;
+      }
+      __syncwarp();
     }
   }
   __shared__ int64_t red[32];
@@ -1234,9 +1282,14 @@ __global__ void k_merge_peers(SrcList L, uint32_t* __restrict__ vis, int64_t nwo
 // First half of the owned-words commit: per-unit counts and degree sums and
 // the tile scan (totals -> ctr->q_count / q_edges, RunStats traversed_edges).
 int launch_commit_count(const PartView& v, const int64_t* off, RunCounters* run, int sms,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool parent_pass = false) {
   const int64_t ntiles = std::max<int64_t>(1, (v.nunits + kScanTile - 1) / kScanTile);
-  k_commit_count<<<resident_grid(k_commit_count, v.nunits * 32, 256, sms), 256, 0, s>>>(v, off);
+  if (parent_pass)
+    k_commit_count<true><<<resident_grid(k_commit_count<true>, v.nunits * 32, 256, sms), 256, 0,
+                           s>>>(v, off);
+  else
+    k_commit_count<false><<<resident_grid(k_commit_count<false>, v.nunits * 32, 256, sms), 256, 0,
+                            s>>>(v, off);
   k_unit_scan_reduce<<<(unsigned)ntiles, 256, 0, s>>>(v);
   k_unit_scan_tiles<<<1, 1024, 0, s>>>(v, ntiles, run);
   return 3;
@@ -1528,6 +1581,17 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   const unsigned small_grid = grid_cap(nwords, 256, sms, 4);
   while (true) {
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
+    // Parents of a single-node top-down level with a large frontier come from
+    // the commit's parent pass instead of phase-1 stores (k_commit_count).
+    // `start` (levels <= L, = `reached`) must be large for the pass's
+    // lowest-neighbour probes to hit without row scans.
+#ifndef BFB_PASS_SHIFT
+#define BFB_PASS_SHIFT 8
+#endif
+    const bool parent_pass = ctx->want_parents && P == 1 && !bottom_up &&
+                             prev_frontier >= std::max<int64_t>(1, n >> 12) &&
+                             reached >= (n >> BFB_PASS_SHIFT);
+    const bool expand_parents = ctx->want_parents && !parent_pass;
     // Phase 1
     const bool part_timing = ctx->timing && P > 1;
     for (int g = 0; g < P; ++g) {
@@ -1540,7 +1604,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
           k_bottom_up<true><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
         else
           k_bottom_up<false><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
-      } else if (ctx->want_parents) {
+      } else if (expand_parents) {
         launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, s);
       } else {
         launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, s);
@@ -1593,7 +1657,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
         if (light)
           launches += launch_commit_light_count(v, off, next_level, ctx->run.p, sms, s);
         else
-          launches += launch_commit_count(v, off, ctx->run.p, sms, s);
+          launches += launch_commit_count(v, off, ctx->run.p, sms, s, parent_pass);
       }
       if (nwords - (p.whi - p.wlo) > 0) {
         k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(v, next_level);

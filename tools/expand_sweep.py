@@ -12,7 +12,7 @@ from paper_2103_13577_b200 import graphs
 scale = int(os.environ.get("SW_SCALE", "29"))
 g = graphs.kronecker(scale, int(os.environ.get("SW_EF", "8")), 1)
 dg = g.device
-roots = graphs.sample_roots(g, 6)
+roots = graphs.sample_roots(g, int(os.environ.get("SW_ROOTS", "6")))
 for parents, direction in ((False, "top-down"), (True, "top-down"), (True, "optimizing"), (False, "optimizing")):
     P = int(os.environ.get("SW_PARTS", "1"))
     dg.setup(dg.partition_1d(P), min(2, P), "butterfly", parents=parents)
