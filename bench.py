@@ -222,9 +222,10 @@ def main():
             exp_ms += st.expand_ms
             exp_launch += st.expand_launches
             # expand algorithmic bytes: 4 B adjacency per edge + 20 B per
-            # frontier vertex (q_pre 8, q_v 4, offsets 8) + 4 B parent per
-            # discovered vertex; summed over levels = per reached vertex
-            level_bytes += 4 * st.traversed_edges + (24 if parents else 20) * st.reached
+            # frontier vertex (q_pre 8, q_base 8, q_v 4); summed over levels =
+            # per reached vertex.  Parents (4 B per vertex) are written by the
+            # commit's parent pass on the dense levels, so they are not counted
+            level_bytes += 4 * st.traversed_edges + 20 * st.reached
         bracket_ms = dg.timer_stop()
     value = hmean(teps)
     peak, peak_src = measured_peaks()
@@ -290,9 +291,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "k_expand (phase 1 top-down expansion)",
-                     "achieved_def": "sum over levels of (4 B x edges + (20 B [+4 B parent]) x "
-                                     "frontier vertices) / "
-                                     "sum of k_expand event time",
+                     "achieved_def": "sum over levels of (4 B x edges + 20 B x frontier "
+                                     "vertices) / sum of k_expand event time",
                      "peak_src": peak_src,
                      "expand_share": round(exp_ms / sum(times), 4),
                      "expand_launches_per_bfs": exp_launch / K,
