@@ -151,6 +151,7 @@ struct PartCounters {
   int64_t frontier;     // |synchronized next frontier| counted at commit
   int64_t pub_count[2]; // published snapshot size, by round parity (phase 2)
   int64_t pub_qpos[2];  // queue-form snapshot fill (device-synchronised mode)
+  int64_t work_next;    // commit write pass: next unit to hand out (dense levels)
 };
 
 // Device-resident run statistics (RunStats).

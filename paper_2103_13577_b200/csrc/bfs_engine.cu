@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(1024) k_unit_scan_tiles(PartView v, int64_t nt
     __syncthreads();
   }
   if (threadIdx.x == 0) {
+    v.ctr->work_next = 0;  // the write pass's unit counter
     v.ctr->q_count = carry_c;
     v.ctr->q_edges = carry_d;
     if (!v.rebuild) atomicAdd((unsigned long long*)&run->traversed_edges, (unsigned long long)carry_d);
@@ -734,6 +735,13 @@ __device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vs
 // current batch's scan and stores, two batches of gathers in flight per warp
 // at 44 registers; the plain build keeps 38 registers and one more CTA per SM
 // for the sparse levels, which are bound by the per-unit bitmap loads.
+constexpr int64_t kUnitChunk = 4;
+__device__ __forceinline__ int64_t grab_units(PartCounters* ctr, int lane) {
+  unsigned long long u = 0;
+  if (lane == 0) u = atomicAdd((unsigned long long*)&ctr->work_next, (unsigned long long)kUnitChunk);
+  return (int64_t)__shfl_sync(0xffffffffu, u, 0);
+}
+
 template <bool kWide, bool kPrefetch>
 __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
                                                       uint32_t next_level, int64_t pf_min) {
@@ -743,7 +751,12 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
   uint16_t* list = s_list[threadIdx.x >> 5];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t unit = gw; unit < v.nunits; unit += nw) {
+  // dense levels: units handed out in chunks from a counter (their work
+  // varies 0..1024 vertices; a static stride left warps idle at the tail)
+  int64_t unit = kPrefetch ? grab_units(v.ctr, lane) : gw;
+  int64_t chunk_end = unit + kUnitChunk;
+  while (unit < v.nunits) {
+    do {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
     unsigned m = __ballot_sync(0xffffffffu, nb != 0);
@@ -821,6 +834,15 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
     if (nb && !v.rebuild) {
       v.start[w0 + lane] = a;
       if (v.front) v.front[w0 + lane] = nb;
+    }
+    } while (0);
+    if (kPrefetch) {
+      if (++unit >= chunk_end) {
+        unit = grab_units(v.ctr, lane);
+        chunk_end = unit + kUnitChunk;
+      }
+    } else {
+      unit += nw;
     }
   }
 }
