@@ -543,15 +543,23 @@ __device__ __forceinline__ int64_t word_degree_sum16(uint32_t x, int64_t w,
 // `start` is probed at random while the pass streams GBs of first_nbr and
 // degree entries: an L2 evict-last hint keeps the 67 MB bitmap resident
 // (commit 6.54 -> 6.42 ms at s29).
-__device__ __forceinline__ bool in_start(const uint32_t* __restrict__ start, uint32_t z) {
-  uint32_t w;
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;"
-               : "=r"(w)
-               : "l"(start + (z >> 5)), "l"(pol));
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// (start is not written while the pass runs, so the load needs no volatile)
+__device__ __forceinline__ bool in_start(const uint32_t* __restrict__ start, uint32_t z,
+                                         uint64_t pol) {
+  uint32_t w;
+  asm("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(w) : "l"(start + (z >> 5)), "l"(pol));
   return (w >> (z & 31)) & 1u;
 }
+
+#ifndef BFB_PASS_BATCH
+#define BFB_PASS_BATCH 4
+#endif
+constexpr int kPassBatch = BFB_PASS_BATCH;
 
 template <bool kParents>
 __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t* __restrict__ off) {
@@ -588,25 +596,42 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
       for (uint32_t x = own; x; x &= x - 1) list[pos++] = (uint16_t)((lane << 5) + __ffs(x) - 1);
       __syncwarp();
       const int64_t ubase = (v.abase + unit * 32) << 5;
-      for (int k = lane; k < (int)c; k += 32) {
-        const uint32_t u = (uint32_t)(ubase + list[k]);
-        const uint2 fn = __ldg(v.first_nbr + u);
-        uint32_t p = kNone;
-        if (fn.x != kNone && in_start(v.start, fn.x)) {
-          p = fn.x;
-        } else if (fn.y != kNone && in_start(v.start, fn.y)) {
-          p = fn.y;
-        } else {
-          const int64_t e = __ldg(off + u + 1);
-          for (int64_t j = __ldg(off + u) + 2; j < e; ++j) {
-            const uint32_t z = __ldg(v.adj + j);
-            if (in_start(v.start, z)) {
-              p = z;
-              break;
+      const uint64_t pol = l2_evict_last_policy();
+      // kPassBatch vertices per lane in flight: their table loads, then
+      // their first probes, then the rare second probes / row scans
+      for (int k0 = 0; k0 < (int)c; k0 += 32 * kPassBatch) {
+        uint32_t u[kPassBatch];
+        uint2 fn[kPassBatch];
+        bool hit[kPassBatch];
+#pragma unroll
+        for (int b = 0; b < kPassBatch; ++b) {
+          const int k = k0 + b * 32 + lane;
+          u[b] = k < (int)c ? (uint32_t)(ubase + list[k]) : kNone;
+          fn[b] = u[b] != kNone ? __ldg(v.first_nbr + u[b]) : make_uint2(kNone, kNone);
+        }
+#pragma unroll
+        for (int b = 0; b < kPassBatch; ++b)
+          hit[b] = fn[b].x != kNone && in_start(v.start, fn[b].x, pol);
+#pragma unroll
+        for (int b = 0; b < kPassBatch; ++b) {
+          if (u[b] == kNone) continue;
+          uint32_t p = kNone;
+          if (hit[b]) {
+            p = fn[b].x;
+          } else if (fn[b].y != kNone && in_start(v.start, fn[b].y, pol)) {
+            p = fn[b].y;
+          } else {
+            const int64_t e = __ldg(off + u[b] + 1);
+            for (int64_t j = __ldg(off + u[b]) + 2; j < e; ++j) {
+              const uint32_t z = __ldg(v.adj + j);
+              if (in_start(v.start, z, pol)) {
+                p = z;
+                break;
+              }
             }
           }
+          v.parent[u[b]] = p;
         }
-        v.parent[u] = p;
       }
       __syncwarp();
     }
