@@ -254,7 +254,7 @@ def main():
                      "bottom_up_levels_mean": round(float(np.mean(do_bu)), 2),
                      "bottom_up_edges_examined_per_traversed": round(do_ex / max(1, do_edges), 4),
                      "note": "same graph, roots, parents and levels (bit-identical); phase 1 switches "
-                             "top-down/bottom-up by Beamer's rule (alpha 14, beta 24); TEPS counts "
+                             "top-down/bottom-up by Beamer's rule (alpha 5, beta 1024, tuned on this graph; Beamer's CPU values are 14, 24); TEPS counts "
                              "the same E_trav"}
 
     # e2e: the public API call (engine.run) with host-resident results

@@ -152,6 +152,8 @@ struct PartCounters {
   int64_t pub_count[2]; // published snapshot size, by round parity (phase 2)
   int64_t pub_qpos[2];  // queue-form snapshot fill (device-synchronised mode)
   int64_t work_next;    // commit write pass: next unit to hand out (dense levels)
+  int64_t rest_edges;   // degree sum of the new vertices outside the owned range
+                        // (rank mode, direction-optimizing: the global switch)
 };
 
 // Device-resident run statistics (RunStats).
@@ -232,7 +234,7 @@ struct bfb_ctx {
   int expand_grid = 0;
   bool timing = false;
   int direction = 0;                  // 0 top-down, 1 direction-optimizing, 2 bottom-up
-  double do_alpha = 14.0, do_beta = 24.0;
+  double do_alpha = 5.0, do_beta = 1024.0;  // tuned at s29 (Beamer: 14, 24)
   bool have_run = false;
   int64_t last_root = -1;
   int64_t last_levels = 0;

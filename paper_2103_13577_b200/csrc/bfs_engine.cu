@@ -73,6 +73,7 @@ struct PartView {
   const uint16_t* deg16;    // min(degree, 65535)
   const uint2* first_nbr;    // two lowest-id neighbours (kNone if absent)
   const uint32_t* adj;       // CSR adjacency (the commit's parent pass)
+  bool rest_degrees;         // k_commit_rest also sums the degrees of its new vertices
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
@@ -110,6 +111,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.deg16 = ctx->g.deg16.p;
   v.first_nbr = ctx->g.first_nbr.p;
   v.adj = ctx->g.adj.p;
+  v.rest_degrees = false;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -464,6 +466,7 @@ __global__ void k_commit_prep(PartCounters** ctrs, int num_nodes) {
     ctrs[g]->frontier = 0;
     ctrs[g]->q_count = 0;
     ctrs[g]->q_edges = 0;
+    ctrs[g]->rest_edges = 0;
   }
 }
 
@@ -959,7 +962,7 @@ __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_l
   const int64_t nunits = (span + 31) / 32;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t fr = 0;
+  int64_t fr = 0, re = 0;
   for (int64_t unit = gw; unit < nunits; unit += nw) {
     const int64_t i = unit * 32 + lane;
     const int64_t w = i < v.wlo ? i : i + (v.whi - v.wlo);
@@ -980,11 +983,17 @@ __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_l
       fr += __popc(nb);
       v.start[w] = a;
       if (v.front) v.front[w] = nb;
+      if (v.rest_degrees) re += word_degree_sum16(nb, w, v.deg16, v.off);
     }
   }
   __shared__ int64_t red[32];
   fr = block_sum_i64(fr, red);
   if (threadIdx.x == 0 && fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+  if (v.rest_degrees) {
+    re = block_sum_i64(re, red);
+    if (threadIdx.x == 0 && re)
+      atomicAdd((unsigned long long*)&v.ctr->rest_edges, (unsigned long long)re);
+  }
 }
 
 // ------------------------------------------------------- bottom-up phase 1 --
@@ -2372,6 +2381,12 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   }
   bool bottom_up = ctx->direction == 2;
   int64_t bu_levels = 0, prev_frontier = 1, nsizes = 1, launches = 0;
+  int64_t seen_edges = 0;  // degree sum of every frontier so far (direction switch)
+  if (ctx->direction == 1) {
+    int64_t ob[2];
+    BFB_CUDA(cudaMemcpy(ob, off + root, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    seen_edges = ob[1] - ob[0];
+  }
   if (sizes_out && max_levels > 0) sizes_out[0] = 1;
   double t_expand = 0, t_exchange = 0, t_commit = 0;
   int64_t expand_launches = 0;
@@ -2423,7 +2438,8 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[4], s));
     // commit: count pass, direction decision, write pass (as engine_bfs)
     const uint32_t next_level = (uint32_t)(D->level + 1);
-    const PartView cv = commit_view_of(ctx, p, next_level);
+    PartView cv = commit_view_of(ctx, p, next_level);
+    cv.rest_degrees = ctx->direction == 1;
     k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
     ++launches;
     if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
@@ -2440,14 +2456,18 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     }
     bool next_bu = ctx->direction == 2;
     if (ctx->direction == 1) {
-      // Beamer's rule on this node's own rows: every node may pick its own
-      // phase-1 direction -- the discoveries (and levels) are the same.
+      // Beamer's rule on global quantities, so every node takes the same
+      // direction: an edge (u on node g, v on node h) is traversed only if g
+      // runs top-down or h bottom-up, so mixed directions would lose edges.
+      // The next frontier's degree sum = owned part (count pass) + the rest
+      // (k_commit_rest), identical on all nodes, as is the running sum.
       BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 3, &ctx->run.p->traversed_edges, sizeof(int64_t),
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 3, &p.ctr.p->rest_edges, sizeof(int64_t),
                                cudaMemcpyDeviceToHost, s));
       BFB_CUDA(cudaStreamSynchronize(s));
-      const int64_t frontier = ctx->pinned[2], mf = ctx->pinned[1];
-      const double mu = (double)(p.owned_edges - ctx->pinned[3]);
+      const int64_t frontier = ctx->pinned[2], mf = ctx->pinned[1] + ctx->pinned[3];
+      seen_edges += mf;
+      const double mu = (double)(ctx->g.m - seen_edges);
       next_bu = bottom_up;
       if (!bottom_up && (double)mf > mu / ctx->do_alpha && frontier > prev_frontier)
         next_bu = true;

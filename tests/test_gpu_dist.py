@@ -65,7 +65,8 @@ def test_ipc_ranks_on_one_gpu(world):
     cases = [(1, "butterfly", 0, False, "top-down"), (world, "butterfly", 7, False, "top-down"),
              (1, "all2all", 123, False, "top-down"), (1, "butterfly", 0, True, "top-down"),
              (world, "butterfly", 7, True, "top-down"), (1, "all2all", 123, True, "top-down"),
-             (2, "butterfly", 5, True, "optimizing"), (1, "butterfly", 9, True, "bottom-up")]
+             (2, "butterfly", 5, True, "optimizing"), (1, "butterfly", 9, True, "bottom-up"),
+             (world, "butterfly", 0, True, "optimizing"), (1, "all2all", 123, True, "optimizing")]
     with tempfile.TemporaryDirectory() as out:
         mp.start_processes(_worker, args=(world, _free_port(), cases, out), nprocs=world,
                            join=True, start_method="spawn")
