@@ -35,6 +35,12 @@ namespace bfb {
 namespace {
 
 constexpr int kExpandBlock = 256;
+// Parent pass (k_commit_count<true>) once this many vertices are reached:
+// n >> BFB_PASS_SHIFT (sweep at s29: shift 4 224.4, 6 226.4, 8 226.9, 10
+// 226.4, always 221.1 GTEP/s).
+#ifndef BFB_PASS_SHIFT
+#define BFB_PASS_SHIFT 8
+#endif
 constexpr int kExpandItems = 8;                // edges per lane per subtile
 constexpr int64_t kSub = 32 * kExpandItems;     // edges per subtile (one warp pass)
 constexpr int kSubPerTile = 8;
@@ -1646,14 +1652,13 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   const unsigned small_grid = grid_cap(nwords, 256, sms, 4);
   while (true) {
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
-    // Parents of a single-node top-down level with a large frontier come from
-    // the commit's parent pass instead of phase-1 stores (k_commit_count).
-    // `start` (levels <= L, = `reached`) must be large for the pass's
-    // lowest-neighbour probes to hit without row scans.
-#ifndef BFB_PASS_SHIFT
-#define BFB_PASS_SHIFT 8
-#endif
-    const bool parent_pass = ctx->want_parents && P == 1 && !bottom_up &&
+    // Parents of a top-down level with a large frontier come from the
+    // commit's parent pass instead of phase-1 stores (k_commit_count): each
+    // node's pass covers its owned new vertices, whoever found them, and the
+    // output takes the min over nodes.  `start` (levels <= L, = `reached`)
+    // must be large for the pass's lowest-neighbour probes to hit without
+    // row scans.
+    const bool parent_pass = ctx->want_parents && !bottom_up &&
                              prev_frontier >= std::max<int64_t>(1, n >> 12) &&
                              reached >= (n >> BFB_PASS_SHIFT);
     const bool expand_parents = ctx->want_parents && !parent_pass;
@@ -2393,6 +2398,12 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   while (true) {
     PartView v = view_of(ctx, p);
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
+    // parent pass as in engine_bfs, decided from global quantities (every
+    // node the same way: the owner's pass covers the vertices that the other
+    // nodes' store-free phase 1 found)
+    const bool parent_pass = ctx->want_parents && !bottom_up &&
+                             prev_frontier >= std::max<int64_t>(1, n >> 12) &&
+                             D->reached >= (n >> BFB_PASS_SHIFT);
     if (bottom_up) {
       const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
       unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
@@ -2401,7 +2412,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       else
         k_bottom_up<false><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
       ++bu_levels;
-    } else if (ctx->want_parents) {
+    } else if (ctx->want_parents && !parent_pass) {
       launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, s);
     } else {
       launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, s);
@@ -2448,7 +2459,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       if (light)
         launches += launch_commit_light_count(cv, off, next_level, ctx->run.p, sms, s);
       else
-        launches += launch_commit_count(cv, off, ctx->run.p, sms, s);
+        launches += launch_commit_count(cv, off, ctx->run.p, sms, s, parent_pass);
     }
     if (nwords - (p.whi - p.wlo) > 0) {
       k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(cv, next_level);
