@@ -187,7 +187,6 @@ struct Part {
   DevBuf<uint32_t> tile_vstart;    // q_local index owning edge t*TILE
   DevBuf<uint32_t> unit_u32;       // commit: owned new vertices per 32-word unit
   DevBuf<int64_t> unit_i64;        // commit: unit degree sums, prefixes, scan tiles
-  DevBuf<uint32_t> dirty;          // sparse levels: bit per commit unit holding a claim
   DevBuf<PartCounters> ctr;
 };
 

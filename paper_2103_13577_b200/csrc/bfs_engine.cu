@@ -80,8 +80,6 @@ struct PartView {
   const uint2* first_nbr;    // two lowest-id neighbours (kNone if absent)
   const uint32_t* adj;       // CSR adjacency (the commit's parent pass)
   bool rest_degrees;         // k_commit_rest also sums the degrees of its new vertices
-  uint32_t* dirty;           // sparse level: commit units with a phase-1 claim (else null)
-  int64_t ndirty;            // words of `dirty`
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
 
@@ -120,8 +118,6 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.first_nbr = ctx->g.first_nbr.p;
   v.adj = ctx->g.adj.p;
   v.rest_degrees = false;
-  v.dirty = nullptr;
-  v.ndirty = (v.nunits + 31) / 32;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -224,14 +220,7 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t* p) {
 // One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
 // with rb the row holding edge r0 and ve the last row that can matter.
 // Returns the row holding edge r0 + kSub (the next subtile's cursor).
-// Sparse levels (kMark): each claim also sets its commit unit's bit in
-// v.dirty (unit = 1024 vertices, single node: units start at vertex 0), so
-// the commit visits only those units instead of the whole bitmap.
-__device__ __forceinline__ void mark_unit(const PartView& v, uint32_t u) {
-  atomicOr(&v.dirty[u >> 15], 1u << ((u >> 10) & 31));
-}
-
-template <bool kParents, bool kMark>
+template <bool kParents>
 __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
                                                    const uint32_t* __restrict__ adj, int64_t r0,
                                                    int span, uint32_t rb, uint32_t ve,
@@ -291,7 +280,6 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
     const uint32_t bit = 1u << (u[it] & 31);
     if (!(wv[it] & bit)) {
       atomicOr(&visited[u[it] >> 5], bit);
-      if (kMark) mark_unit(v, u[it]);
       if (kParents) {
         const uint32_t ro = (rows[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
         v.parent[u[it]] = __ldg(v.q_v + vs + ro);
@@ -306,7 +294,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
 // kRunItems probes in flight.
 constexpr int kRunItems = 12;  // measured at s29 (parents on): 8 -> 218.7, 12 -> 219.1, 16 -> 217.7 GTEP/s
 
-template <bool kParents, bool kMark>
+template <bool kParents>
 __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t* __restrict__ adj,
                                                int64_t e0, int span, uint32_t row, uint64_t pol) {
   const int lane = threadIdx.x & 31;
@@ -330,7 +318,6 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
       const uint32_t bit = 1u << (u[it] & 31);
       if (!(wv[it] & bit)) {
         atomicOr(&visited[u[it] >> 5], bit);
-        if (kMark) mark_unit(v, u[it]);
         if (kParents) v.parent[u[it]] = src;
       }
     }
@@ -357,7 +344,7 @@ __device__ __forceinline__ uint32_t find_row(const int64_t* __restrict__ q_pre, 
   return lo;
 }
 
-template <bool kParents, bool kMark>
+template <bool kParents>
 __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
     k_expand_w(PartView v, const uint32_t* __restrict__ adj) {
   const int64_t T = v.ctr->q_edges;
@@ -376,11 +363,11 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       uint32_t cur = v.tile_vstart[t];
       if (cur == ve) {  // the whole tile inside one row
-        expand_row_run<kParents, kMark>(v, adj, e0, span, cur, pol);
+        expand_row_run<kParents>(v, adj, e0, span, cur, pol);
         continue;
       }
       for (int k = 0; k * kSub < span; ++k)
-        cur = expand_subtile<kParents, kMark>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
+        cur = expand_subtile<kParents>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
                                        cur, ve, le_mask, pol);
     }
   } else {
@@ -391,7 +378,7 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const uint32_t vs = v.tile_vstart[t];
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       const uint32_t cur = (st % kSubPerTile) ? find_row(v.q_pre, vs, ve, r0) : vs;
-      expand_subtile<kParents, kMark>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask, pol);
+      expand_subtile<kParents>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask, pol);
     }
   }
 }
@@ -399,16 +386,12 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
 // Launch phase 1 (top-down) for one part on stream s.
 template <bool kParents>
 void launch_expand(int grid, const PartView& v, const uint32_t* adj, cudaStream_t s) {
-  if (v.dirty)
-    k_expand_w<kParents, true><<<grid, kExpandBlock, 0, s>>>(v, adj);
-  else
-    k_expand_w<kParents, false><<<grid, kExpandBlock, 0, s>>>(v, adj);
+  k_expand_w<kParents><<<grid, kExpandBlock, 0, s>>>(v, adj);
 }
 
 template <bool kParents>
 int expand_occupancy(int* occ) {
-  BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents, false>,
-                                                         kExpandBlock, 0));
+  BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents>, kExpandBlock, 0));
   return BFB_OK;
 }
 
@@ -582,23 +565,12 @@ __device__ __forceinline__ bool in_start(const uint32_t* __restrict__ start, uin
   return (w >> (z & 31)) & 1u;
 }
 
-// Sparse levels: units whose `dirty` bit is clear hold no claim of this
-// level, and the commit passes skip them after one (L1-resident) bit test.
-// The units stay strided over the warps, so the dirty ones spread evenly.
-// Dirty bits are a superset hint: a clean unit visited costs time, never a
-// wrong result.
-__device__ __forceinline__ bool unit_clean(const PartView& v, int64_t unit) {
-  return !((v.dirty[unit >> 5] >> (unit & 31)) & 1u);
-}
-
 #ifndef BFB_PASS_BATCH
 #define BFB_PASS_BATCH 4
 #endif
 constexpr int kPassBatch = BFB_PASS_BATCH;
 
-// kSparse: only the units of v.dirty (the caller zeroed this level's
-// lvbits slice and the unit counts first).
-template <bool kParents, bool kSparse>
+template <bool kParents>
 __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t* __restrict__ off) {
   __shared__ uint16_t s_list[kParents ? 256 / 32 : 1][kParents ? 1024 : 1];
   const int lane = threadIdx.x & 31;
@@ -606,7 +578,6 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t fr = 0;
   for (int64_t unit = gw; unit < v.nunits; unit += nw) {
-    if (kSparse && unit_clean(v, unit)) continue;
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
     if (!v.rebuild) fr += __popc(nb);  // a rebuild's frontier was counted by its level's commit
@@ -808,7 +779,7 @@ __device__ __forceinline__ int64_t grab_units(PartCounters* ctr, int lane) {
 template <bool kWide, bool kPrefetch>
 __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
                                                       uint32_t next_level, int64_t pf_min) {
-  if ((!v.dirty && v.ctr->q_count >= pf_min) != kPrefetch) return;
+  if ((v.ctr->q_count >= pf_min) != kPrefetch) return;
   __shared__ uint16_t s_list[256 / 32][1024];  // unit-local vertex index (word * 32 + bit)
   const int lane = threadIdx.x & 31;
   uint16_t* list = s_list[threadIdx.x >> 5];
@@ -816,12 +787,10 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   // dense levels: units handed out in chunks from a counter (their work
   // varies 0..1024 vertices; a static stride left warps idle at the tail)
-  const bool sparse = !kPrefetch && v.dirty;  // sparse level: dirty units only
   int64_t unit = kPrefetch ? grab_units(v.ctr, lane) : gw;
   int64_t chunk_end = unit + kUnitChunk;
   while (unit < v.nunits) {
     do {
-    if (sparse && unit_clean(v, unit)) continue;
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
     unsigned m = __ballot_sync(0xffffffffu, nb != 0);
@@ -1386,23 +1355,12 @@ __global__ void k_merge_peers(SrcList L, uint32_t* __restrict__ vis, int64_t nwo
 int launch_commit_count(const PartView& v, const int64_t* off, RunCounters* run, int sms,
                         cudaStream_t s, bool parent_pass = false) {
   const int64_t ntiles = std::max<int64_t>(1, (v.nunits + kScanTile - 1) / kScanTile);
-  if (v.dirty) {  // sparse level: zero what the full pass would write, visit the dirty units
-    if (v.lvbits)
-      BFB_CUDA(cudaMemsetAsync(v.lvbits + v.wlo, 0, (v.whi - v.wlo) * sizeof(uint32_t), s));
-    BFB_CUDA(cudaMemsetAsync(v.ucnt, 0, v.nunits * sizeof(uint32_t), s));
-    BFB_CUDA(cudaMemsetAsync(v.udeg, 0, v.nunits * sizeof(int64_t), s));
-    k_commit_count<false, true><<<resident_grid(k_commit_count<false, true>, v.nunits * 32, 256,
-                                                sms),
-                                  256, 0, s>>>(v, off);
-  } else if (parent_pass) {
-    k_commit_count<true, false><<<resident_grid(k_commit_count<true, false>, v.nunits * 32, 256,
-                                                sms),
-                                  256, 0, s>>>(v, off);
-  } else {
-    k_commit_count<false, false><<<resident_grid(k_commit_count<false, false>, v.nunits * 32, 256,
-                                                 sms),
-                                   256, 0, s>>>(v, off);
-  }
+  if (parent_pass)
+    k_commit_count<true><<<resident_grid(k_commit_count<true>, v.nunits * 32, 256, sms), 256, 0,
+                           s>>>(v, off);
+  else
+    k_commit_count<false><<<resident_grid(k_commit_count<false>, v.nunits * 32, 256, sms), 256, 0,
+                            s>>>(v, off);
   k_unit_scan_reduce<<<(unsigned)ntiles, 256, 0, s>>>(v);
   k_unit_scan_tiles<<<1, 1024, 0, s>>>(v, ntiles, run);
   return 3;
@@ -1574,8 +1532,6 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
       const int64_t ntiles = (nunits + kScanTile - 1) / kScanTile + 1;
       BFB_TRY(p.unit_u32.alloc(nunits));
       BFB_TRY(p.unit_i64.alloc(3 * nunits + 2 * ntiles));
-      BFB_TRY(p.dirty.alloc((nunits + 31) / 32 + 1));
-      BFB_CUDA(cudaMemset(p.dirty.p, 0, p.dirty.n * sizeof(uint32_t)));
     }
     BFB_TRY(p.ctr.alloc(1));
     BFB_CUDA(cudaMemset(p.visited.p, 0, nwords_pad * sizeof(uint32_t)));
@@ -1702,10 +1658,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     // output takes the min over nodes.  `start` (levels <= L, = `reached`)
     // must be large for the pass's lowest-neighbour probes to hit without
     // row scans.
-    // Sparse level (single node, small top-down frontier): phase 1 marks the
-    // commit units it claims in, and the commit visits only those.
-    const bool sparse = P == 1 && !bottom_up && prev_frontier < std::max<int64_t>(64, n >> 14);
-    const bool parent_pass = ctx->want_parents && !bottom_up && !sparse &&
+    const bool parent_pass = ctx->want_parents && !bottom_up &&
                              prev_frontier >= std::max<int64_t>(1, n >> 12) &&
                              reached >= (n >> BFB_PASS_SHIFT);
     const bool expand_parents = ctx->want_parents && !parent_pass;
@@ -1714,10 +1667,6 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     for (int g = 0; g < P; ++g) {
       if (part_timing) BFB_CUDA(cudaEventRecord(D->part_ev[g], s));
       PartView v = view_of(ctx, ctx->parts[g]);
-      if (sparse) {
-        v.dirty = ctx->parts[g].dirty.p;
-        BFB_CUDA(cudaMemsetAsync(v.dirty, 0, ctx->parts[g].dirty.n * sizeof(uint32_t), s));
-      }
       if (bottom_up) {
         const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
         unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
@@ -1774,7 +1723,6 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     for (int g = 0; g < P; ++g) {
       Part& p = ctx->parts[g];
       PartView v = commit_view_of(ctx, p, next_level);
-      if (sparse) v.dirty = p.dirty.p;
       if (p.whi > p.wlo) {
         if (light)
           launches += launch_commit_light_count(v, off, next_level, ctx->run.p, sms, s);
@@ -1820,9 +1768,8 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
           launches += launch_commit_rebuild(commit_view_of(ctx, p, next_level), off, next_level,
                                             ctx->run.p, sms, s);
       } else {
-        PartView wv = commit_view_of(ctx, p, next_level);
-        if (sparse) wv.dirty = p.dirty.p;
-        launches += launch_commit_write(wv, off, next_level, !next_bu, sms, s);
+        launches += launch_commit_write(commit_view_of(ctx, p, next_level), off, next_level,
+                                        !next_bu, sms, s);
       }
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
