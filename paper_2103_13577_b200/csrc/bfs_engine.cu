@@ -1112,15 +1112,26 @@ __device__ __forceinline__ void load_level_slices(const uint32_t* __restrict__ l
   for (int k = 0; k < 5; ++k) L.s[k] = 0u;
   L.any = 0u;
   if (in) {
-    // fully unrolled: the level's bits are compile-time, one OR per set bit
+    // groups of 8 levels: the group's loads issue together, then fold; fully
+    // unrolled, so each level's bits are compile-time (one OR per set bit)
 #pragma unroll
-    for (int l = 1; l < kLevelBits; ++l) {
-      if (l > nl) break;
-      const uint32_t x = __ldg(lvbits + l * pad + wk);
-      L.any |= x;
+    for (int g0 = 1; g0 < kLevelBits; g0 += 8) {
+      if (g0 > nl) break;
+      uint32_t x[8];
 #pragma unroll
-      for (int k = 0; k < 5; ++k)
-        if ((l >> k) & 1) L.s[k] |= x;
+      for (int j = 0; j < 8; ++j) {
+        const int l = g0 + j;
+        x[j] = (l < kLevelBits && l <= nl) ? __ldg(lvbits + l * pad + wk) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int l = g0 + j;
+        if (l >= kLevelBits) break;
+        L.any |= x[j];
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+          if ((l >> k) & 1) L.s[k] |= x[j];
+      }
     }
   }
   L.vis = in ? __ldg(visited + wk) : 0u;
