@@ -57,3 +57,15 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_levels_readout_bytes():
+    """bench.py's e2e d2h accounting mirrors csrc/host_out.cu read_levels:
+    4 bits per vertex up to 15 levels (15 = UNREACHED), 8 up to 255, else 32."""
+    from paper_2103_13577_b200.device import levels_readout_bytes
+
+    assert levels_readout_bytes(1 << 29, 8) == 1 << 28
+    assert levels_readout_bytes(7, 15) == 4
+    assert levels_readout_bytes(7, 16) == 7
+    assert levels_readout_bytes(1000, 255) == 1000
+    assert levels_readout_bytes(1000, 256) == 4000
