@@ -769,7 +769,11 @@ __device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vs
 // current batch's scan and stores, two batches of gathers in flight per warp
 // at 44 registers; the plain build keeps 38 registers and one more CTA per SM
 // for the sparse levels, which are bound by the per-unit bitmap loads.
-constexpr int64_t kUnitChunk = 4;
+// units per counter grab (s29 commit: 1 -> 6.05, 2 -> 5.56, 4 -> 5.48, 8 -> 5.55, 16 -> 5.68 ms)
+#ifndef BFB_UNIT_CHUNK
+#define BFB_UNIT_CHUNK 4
+#endif
+constexpr int64_t kUnitChunk = BFB_UNIT_CHUNK;
 __device__ __forceinline__ int64_t grab_units(PartCounters* ctr, int lane) {
   unsigned long long u = 0;
   if (lane == 0) u = atomicAdd((unsigned long long*)&ctr->work_next, (unsigned long long)kUnitChunk);
