@@ -472,6 +472,7 @@ __global__ void k_commit_prep(PartCounters** ctrs, int num_nodes) {
     ctrs[g]->frontier = 0;
     ctrs[g]->q_count = 0;
     ctrs[g]->q_edges = 0;
+    ctrs[g]->work_next = 0;  // the count pass's unit counter (parent pass)
     ctrs[g]->rest_edges = 0;
   }
 }
@@ -565,6 +566,17 @@ __device__ __forceinline__ bool in_start(const uint32_t* __restrict__ start, uin
   return (w >> (z & 31)) & 1u;
 }
 
+// units per counter grab (s29 commit: 1 -> 6.05, 2 -> 5.56, 4 -> 5.48, 8 -> 5.55, 16 -> 5.68 ms)
+#ifndef BFB_UNIT_CHUNK
+#define BFB_UNIT_CHUNK 4
+#endif
+constexpr int64_t kUnitChunk = BFB_UNIT_CHUNK;
+__device__ __forceinline__ int64_t grab_units(PartCounters* ctr, int lane) {
+  unsigned long long u = 0;
+  if (lane == 0) u = atomicAdd((unsigned long long*)&ctr->work_next, (unsigned long long)kUnitChunk);
+  return (int64_t)__shfl_sync(0xffffffffu, u, 0);
+}
+
 #ifndef BFB_PASS_BATCH
 #define BFB_PASS_BATCH 4
 #endif
@@ -577,7 +589,11 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t fr = 0;
-  for (int64_t unit = gw; unit < v.nunits; unit += nw) {
+  // with the parent pass a unit's work varies with its new vertices: units
+  // are handed out in chunks from a counter (zeroed by k_commit_prep)
+  int64_t unit = kParents ? grab_units(v.ctr, lane) : gw;
+  int64_t chunk_end = unit + kUnitChunk;
+  while (unit < v.nunits) {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
     if (!v.rebuild) fr += __popc(nb);  // a rebuild's frontier was counted by its level's commit
@@ -643,6 +659,14 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
         }
       }
       __syncwarp();
+    }
+    if (kParents) {
+      if (++unit >= chunk_end) {
+        unit = grab_units(v.ctr, lane);
+        chunk_end = unit + kUnitChunk;
+      }
+    } else {
+      unit += nw;
     }
   }
   __shared__ int64_t red[32];
@@ -769,17 +793,6 @@ __device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vs
 // current batch's scan and stores, two batches of gathers in flight per warp
 // at 44 registers; the plain build keeps 38 registers and one more CTA per SM
 // for the sparse levels, which are bound by the per-unit bitmap loads.
-// units per counter grab (s29 commit: 1 -> 6.05, 2 -> 5.56, 4 -> 5.48, 8 -> 5.55, 16 -> 5.68 ms)
-#ifndef BFB_UNIT_CHUNK
-#define BFB_UNIT_CHUNK 4
-#endif
-constexpr int64_t kUnitChunk = BFB_UNIT_CHUNK;
-__device__ __forceinline__ int64_t grab_units(PartCounters* ctr, int lane) {
-  unsigned long long u = 0;
-  if (lane == 0) u = atomicAdd((unsigned long long*)&ctr->work_next, (unsigned long long)kUnitChunk);
-  return (int64_t)__shfl_sync(0xffffffffu, u, 0);
-}
-
 template <bool kWide, bool kPrefetch>
 __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
                                                       uint32_t next_level, int64_t pf_min) {
