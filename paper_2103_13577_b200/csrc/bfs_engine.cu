@@ -473,6 +473,7 @@ __global__ void k_commit_prep(PartCounters** ctrs, int num_nodes) {
     ctrs[g]->q_count = 0;
     ctrs[g]->q_edges = 0;
     ctrs[g]->work_next = 0;  // the count pass's unit counter (parent pass)
+    ctrs[g]->bu_next = 0;    // the next level's bottom-up group counter
     ctrs[g]->rest_edges = 0;
   }
 }
@@ -1036,13 +1037,19 @@ template <bool kParents>
 __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* __restrict__ adj,
                                                    unsigned long long* examined) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t* __restrict__ front = v.front;
   unsigned long long ex = 0;
   // 32 words per step: lane k reads word k's visited / non-isolated bits
   // (one coalesced load each), then the warp walks the words with candidates
-  for (int64_t w0 = v.wlo + gw * 32; w0 < v.whi; w0 += nw * 32) {
+  // Groups are handed out from a counter (zeroed by k_commit_prep): the
+  // candidates' row scans vary widely, and a static stride left most warps
+  // idle behind the slowest (s29 DO 892 -> 954 GTEP/s).
+  auto grab = [&]() -> int64_t {
+    unsigned long long g = 0;
+    if (lane == 0) g = atomicAdd((unsigned long long*)&v.ctr->bu_next, 1ull);
+    return v.wlo + 32 * (int64_t)__shfl_sync(0xffffffffu, g, 0);
+  };
+  for (int64_t w0 = grab(); w0 < v.whi; w0 = grab()) {
     const int64_t wk = w0 + lane;
     const uint32_t vis_k = wk < v.whi ? v.visited[wk] : 0xFFFFFFFFu;
     const uint32_t cand_k = wk < v.whi ? owned_mask(wk, v.lo, v.hi) & ~vis_k & v.nonisol[wk] : 0u;
