@@ -153,6 +153,7 @@ struct PartCounters {
   int64_t pub_qpos[2];  // queue-form snapshot fill (device-synchronised mode)
   int64_t work_next;    // commit write pass: next unit to hand out (dense levels)
   int64_t bu_next;      // bottom-up phase 1: next 32-word group to hand out
+  int64_t ex_next;      // top-down phase 1: next tile to hand out (dense levels)
   int64_t rest_edges;   // degree sum of the new vertices outside the owned range
                         // (rank mode, direction-optimizing: the global switch)
 };

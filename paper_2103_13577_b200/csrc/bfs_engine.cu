@@ -357,7 +357,16 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_evict_first_policy();
   if (ntiles >= nwarps) {
-    for (int64_t t = gw; t < ntiles; t += nwarps) {
+    // tiles handed out from a counter (zeroed by k_commit_prep): hub tiles
+    // (run path) and row-resolving tiles differ in cost, and with a static
+    // stride the warps that drew the slow ones set the level's tail
+    // (s29: expand 30.6 -> 29.3 ms)
+    auto grab = [&]() -> int64_t {
+      unsigned long long g = 0;
+      if (lane == 0) g = atomicAdd((unsigned long long*)&v.ctr->ex_next, 1ull);
+      return (int64_t)__shfl_sync(0xffffffffu, g, 0);
+    };
+    for (int64_t t = grab(); t < ntiles; t = grab()) {
       const int64_t e0 = t * kTile;
       const int span = (int)min(kTile, T - e0);
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
@@ -474,6 +483,7 @@ __global__ void k_commit_prep(PartCounters** ctrs, int num_nodes) {
     ctrs[g]->q_edges = 0;
     ctrs[g]->work_next = 0;  // the count pass's unit counter (parent pass)
     ctrs[g]->bu_next = 0;    // the next level's bottom-up group counter
+    ctrs[g]->ex_next = 0;    // the next level's top-down tile counter
     ctrs[g]->rest_edges = 0;
   }
 }
