@@ -292,7 +292,10 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
 // A tile lying inside one row (hub rows: most of the edges of the hub-heavy
 // early levels): no row resolution, no per-batch q loads, and each lane keeps
 // kRunItems probes in flight.
-constexpr int kRunItems = 12;  // measured at s29 (parents on): 8 -> 218.7, 12 -> 219.1, 16 -> 217.7 GTEP/s
+#ifndef BFB_RUN_ITEMS
+#define BFB_RUN_ITEMS 16
+#endif
+constexpr int kRunItems = BFB_RUN_ITEMS;  // s29 TD, tiles from a counter: 8 241.2, 12 241.3, 16 243.5, 20 242.6, 24 241.0 GTEP/s
 
 template <bool kParents>
 __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t* __restrict__ adj,
