@@ -36,10 +36,11 @@ namespace {
 
 constexpr int kExpandBlock = 256;
 // Parent pass (k_commit_count<true>) once this many vertices are reached:
-// n >> BFB_PASS_SHIFT (sweep at s29: shift 4 224.4, 6 226.4, 8 226.9, 10
-// 226.4, always 221.1 GTEP/s).
+// n >> BFB_PASS_SHIFT (s29 sweeps: first pass build 4 224.4, 6 226.4, 8
+// 226.9, 10 226.4, always 221.1 GTEP/s; with the batched, counter-scheduled
+// pass and expand 8 243.6, 10 245.4, 12 245.0, 16 244.0).
 #ifndef BFB_PASS_SHIFT
-#define BFB_PASS_SHIFT 8
+#define BFB_PASS_SHIFT 12
 #endif
 constexpr int kExpandItems = 8;                // edges per lane per subtile
 constexpr int64_t kSub = 32 * kExpandItems;     // edges per subtile (one warp pass)
