@@ -1,17 +1,20 @@
-"""ButterFly BFS benchmark (driver contract).
+"""ButterFly BFS benchmark (driver contract; see DESIGN.md §5 Measurement).
 
 Workload: Kronecker scale 29, edge factor 8, seed 1 (BASELINE.json config 5),
-built on device; 64 Graph500 roots (default_rng(2103) over non-isolated
-vertices).  A step = one BFS from the next root (top-down ButterFly BFS,
-parents on), the graph resident in HBM.  Metric = harmonic mean over the
-timed roots of E_trav / t (GTEP/s), E_trav = sum of degrees of reached
-vertices, t = device time from root injection to termination.
+built on device; the 64 Graph500 roots (default_rng(2103) over non-isolated
+vertices).  ONE STEP = one pass over all 64 roots (64 top-down ButterFly
+BFSs, parents on), the graph resident in HBM -- so every run times every
+root.  Metric = harmonic mean over the timed BFSs of E_trav / t (GTEP/s),
+E_trav = sum of degrees of the reached vertices, t = device time from root
+injection to termination (levels and parents final on device).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU; fails if fewer than N GPUs are visible).
 --impl reference times the reference's CPU path (oracle/bfs_omp.c: the
-bfs-oracle of SPEC.md restated in C + OpenMP, on every host thread) on the
-graph copied to host.
+bfs-oracle of SPEC.md restated in C + OpenMP, every host thread), one
+COMPLETE BFS per step from the next root, on the graph copied to host.
 """
 
 from __future__ import annotations
@@ -19,6 +22,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,20 +36,23 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BFS GTEP/s (harmonic mean, 64 roots) Kronecker s29 ef8 at 1/2/4/8 B200"
 UNIT = "GTEP/s"
+# algorithmic phase-1 bytes: 4 B of adjacency per traversed edge and 20 B per
+# frontier vertex (q_pre 8, q_base 8, q_v 4); summed over levels = per reached
+# vertex (parents come from the commit's parent pass on the dense levels)
+BYTES_PER_EDGE, BYTES_PER_VERTEX = 4, 20
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
-    ap.add_argument("--steps", type=int, default=64)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5, help="timed passes over the roots")
+    ap.add_argument("--warmup", type=int, default=3, help="untimed passes over the roots")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=29)
     ap.add_argument("--edge-factor", type=int, default=8)
     ap.add_argument("--fanout", type=int, default=0, help="0 = min(2, N)")
     ap.add_argument("--roots", type=int, default=64)
-    ap.add_argument("--e2e-steps", type=int, default=8)
-    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
+    ap.add_argument("--cpu-roots", type=int, default=2, help="complete CPU BFSs for cpu_baseline")
     ap.add_argument("--no-parents", action="store_true")
     return ap.parse_args()
 
@@ -117,7 +124,8 @@ def measured_peaks():
 
 
 def committed_traffic(scale, ef):
-    """DRAM bytes per expand launch from the committed ncu capture, if any."""
+    """(DRAM bytes per expand launch, bytes per expand launch algorithmic,
+    source) from the committed ncu launch list of one s29 BFS, if any."""
     p = os.path.join(ROOT, "profiles", "expand_traffic.json")
     if not os.path.exists(p):
         return None
@@ -134,6 +142,35 @@ def dist_env():
     return ws, rank, local
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n):
+    """--gpus N without torchrun: re-launch this script as N ranks (one per
+    GPU).  BFB_SHARED_GPU=1 (with BFB_DIST_BACKEND=gloo) lets the ranks share
+    cuda:0, for protocol runs on a one-GPU box."""
+    import torch
+
+    have = torch.cuda.device_count()
+    shared = os.environ.get("BFB_SHARED_GPU") == "1"
+    if have < n and not shared:
+        print(json.dumps({"error": f"--gpus {n} requested but only {have} GPU(s) visible"}),
+              flush=True)
+        return 2
+    env = dict(os.environ)
+    if shared:
+        env["BFB_DEVICE"] = "0"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def hmean(xs):
     xs = [x for x in xs if x > 0]
     return len(xs) / sum(1.0 / x for x in xs) if xs else 0.0
@@ -144,191 +181,213 @@ def cpu_threads():
     return len(os.sched_getaffinity(0))
 
 
-def cpu_sample(off, adj, roots, budget_s, steps):
-    """Reference CPU path on bounded samples: the oracle's top-down BFS
-    restated in C + OpenMP (oracle/bfs_omp.c, the paper's
-    OpenMP worker model) on every host thread; each step runs a BFS from the
-    next root, stopping after budget_s / steps seconds; returns per-step
-    (GTEP/s = edges scanned / time, edges, seconds, completed)."""
+def cpu_complete_bfs(off, adj, root):
+    """The reference CPU path for one root: a COMPLETE top-down BFS by
+    oracle/bfs_omp.c (SPEC.md:136-163 restated in C + OpenMP, the paper's
+    OpenMP worker model) on every host thread.  Returns (levels, GTEP/s,
+    seconds), GTEP/s = E_trav / time."""
     from oracle import cbfs
 
-    per = max(0.5, budget_s / max(1, steps))
-    out = []
-    for i in range(steps):
-        _, scanned, secs, done = cbfs.bfs_top_down(off, adj, int(roots[i % len(roots)]),
-                                                   time_budget_s=per, threads=cpu_threads())
-        out.append((scanned / secs / 1e9 if secs > 0 else 0.0, scanned, secs, done))
-    return out
+    t = time.perf_counter()
+    d = cbfs.bfs_top_down(off, adj, int(root), threads=cpu_threads())
+    secs = time.perf_counter() - t
+    deg = np.diff(off)
+    e = int(deg[d != 0xFFFFFFFF].sum())
+    return d, e / secs / 1e9, secs
 
 
-def host_csr(dg):
-    t = time.time()
-    off, adj = dg.csr()
-    return off, adj, time.time() - t
+def sha16(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def cpu_baseline_leg(off, adj, roots, gpu_sha, copy_s):
+    """cpu_baseline (untimed for the GPU line): complete CPU BFSs from the
+    first roots, their levels compared with the GPU's for the same roots."""
+    res = [cpu_complete_bfs(off, adj, r) for r in roots]
+    match = all(sha16(d) == gpu_sha[int(r)] for (d, _, _), r in zip(res, roots))
+    return {"value": round(hmean([x[1] for x in res]), 5), "unit": UNIT, "cores": cpu_threads(),
+            "kind": "port",
+            "sample": f"{len(roots)} complete top-down BFSs (roots {[int(r) for r in roots]}) by "
+                      f"oracle/bfs_omp.c (C + OpenMP, {cpu_threads()} threads) on the same CSR "
+                      f"copied to host ({copy_s:.1f} s), GTEP/s = E_trav / time, "
+                      f"{sum(x[2] for x in res):.1f} s of CPU BFS",
+            "levels_match_gpu": bool(match),
+            "host_threads_available": cpu_threads()}
+
+
+# ------------------------------------------------------------ the JSON line --
+def base_line(args, cfg, n_gpus, K, W, value, bracket_ms):
+    return {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": n_gpus, "steps": K,
+        "warmup": W, "ms_per_step": round(bracket_ms / K, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": cfg,
+    }
+
+
+def config_of(args, n_gpus, fanout, parents):
+    return {
+        "workload": f"kronecker s{args.scale} ef{args.edge_factor} seed1, {args.roots} Graph500 "
+                    "roots, top-down ButterFly BFS; one step = one pass over all the roots "
+                    f"({args.roots} BFSs)",
+        "scale": args.scale, "edge_factor": args.edge_factor, "seed": 1, "roots": args.roots,
+        "roots_timed": args.roots, "num_parts": n_gpus, "fanout": fanout, "strategy": "butterfly",
+        "parents": parents, "parallelism": f"1D vertex partition x{n_gpus}",
+        "l2": "inputs larger than L2 (CSR of s29 ~38 GB vs 126 MB L2)",
+        "graph_build": "on device (bit-exact generator, CSR, partition)",
+    }
 
 
 # ------------------------------------------------------------------- main ---
 def main():
     args = parse()
     ws, rank, local = dist_env()
-    n_gpus = max(args.gpus, ws)
-    fanout = args.fanout or min(2, n_gpus)
-    parents = not args.no_parents
-    cfg = {
-        "workload": f"kronecker s{args.scale} ef{args.edge_factor} seed1, {args.roots} Graph500 roots, "
-                    "top-down ButterFly BFS (one step = one BFS)",
-        "scale": args.scale, "edge_factor": args.edge_factor, "seed": 1, "roots": args.roots,
-        "num_parts": n_gpus, "fanout": fanout, "strategy": "butterfly", "parents": parents,
-        "parallelism": f"1D vertex partition x{n_gpus}",
-        "l2": "inputs larger than L2 (CSR of s29 ~38 GB vs 126 MB L2)",
-        "graph_build": "on device (bit-exact generator, CSR, partition)",
-    }
-
     if args.impl == "reference":
-        if rank != 0:
-            return
-        run_reference(args, cfg, n_gpus)
-        return
-
+        if rank == 0:
+            run_reference(args, max(args.gpus, ws))
+        return 0
+    if ws == 1 and args.gpus > 1:
+        return spawn_ranks(args.gpus)
     if ws > 1:
-        line = main_rank(args, cfg)
-        if rank == 0 and line is not None:
-            print(json.dumps(line), flush=True)
-        return
+        line = main_rank(args)
+    else:
+        line = main_single(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    return 0
 
+
+def main_single(args):
     from paper_2103_13577_b200 import engine, graphs
     from paper_2103_13577_b200.device import levels_readout_bytes
 
+    _, _, local = dist_env()
+    parents = not args.no_parents
+    cfg = config_of(args, 1, 1, parents)
     t0 = time.time()
     g = graphs.kronecker(args.scale, args.edge_factor, 1, device=local)
     dg = g.device
     build_s = time.time() - t0
-    roots = graphs.sample_roots(g, args.roots)
+    roots = [int(r) for r in graphs.sample_roots(g, args.roots)]
     dg.setup(dg.partition_1d(1), 1, "butterfly", parents=parents)
     dg.set_timing(True)
     K, W = args.steps, args.warmup
-    for i in range(W):
-        dg.bfs(int(roots[(K + i) % len(roots)]), levels=False)
-    teps, times, edges, launches = [], [], [], 0
-    exp_ms, exp_launch, level_bytes = 0.0, 0, 0
+
+    def passes(count, record):
+        for _ in range(count):
+            for r in roots:
+                _, _, _, st, _ = dg.bfs(r, levels=False)
+                if record is not None:
+                    record.append(st)
+
+    passes(W, None)
+    td = []
     with ClockSampler(local) as clk:
         dg.timer_start()
-        for i in range(K):
-            _, _, sizes, st, _ = dg.bfs(int(roots[i % len(roots)]), levels=False)
-            teps.append(st.traversed_edges / (st.elapsed_ms * 1e-3) / 1e9)
-            times.append(st.elapsed_ms)
-            edges.append(st.traversed_edges)
-            launches += st.kernel_launches
-            exp_ms += st.expand_ms
-            exp_launch += st.expand_launches
-            # expand algorithmic bytes: 4 B adjacency per edge + 20 B per
-            # frontier vertex (q_pre 8, q_base 8, q_v 4); summed over levels =
-            # per reached vertex.  Parents (4 B per vertex) are written by the
-            # commit's parent pass on the dense levels, so they are not counted
-            level_bytes += 4 * st.traversed_edges + 20 * st.reached
+        passes(K, td)
         bracket_ms = dg.timer_stop()
+    teps = [st.traversed_edges / (st.elapsed_ms * 1e-3) / 1e9 for st in td]
     value = hmean(teps)
+    exp_ms = sum(st.expand_ms for st in td)
+    edges = sum(st.traversed_edges for st in td)
+    level_bytes = sum(BYTES_PER_EDGE * st.traversed_edges + BYTES_PER_VERTEX * st.reached
+                      for st in td)
+    launches = sum(st.kernel_launches for st in td)
+    exp_launch = sum(st.expand_launches for st in td)
     peak, peak_src = measured_peaks()
-    # the expand's real ceiling: one random visited-bitmap probe per edge
     probe_peak = dg.probe_peak((g.num_vertices + 7) // 8)
-    probe_achieved = sum(edges) / (exp_ms * 1e-3)
     achieved = level_bytes / (exp_ms * 1e-3) / 1e9 if exp_ms > 0 else 0.0
-    traffic = committed_traffic(args.scale, args.edge_factor)
 
     # Direction-optimizing phase 1 (paper contribution 3; SURVEY §8 f4) on the
     # same roots -- reported beside the top-down headline, not instead of it.
     dg.set_direction("optimizing")
-    for i in range(W):
-        dg.bfs(int(roots[(K + i) % len(roots)]), levels=False)
-    do_teps, do_ms, do_bu, do_ex, do_edges = [], [], [], 0, 0
-    for i in range(K):
-        _, _, _, st, _ = dg.bfs(int(roots[i % len(roots)]), levels=False)
-        do_teps.append(st.traversed_edges / (st.elapsed_ms * 1e-3) / 1e9)
-        do_ms.append(st.elapsed_ms)
-        do_bu.append(st.bottom_up_levels)
-        do_ex += st.edges_examined
-        do_edges += st.traversed_edges
+    passes(1, None)
+    do = []
+    passes(K, do)
     dg.set_direction("top-down")
-    direction_opt = {"value": round(hmean(do_teps), 3), "unit": UNIT,
-                     "bfs_ms_mean": round(float(np.mean(do_ms)), 4),
-                     "bottom_up_levels_mean": round(float(np.mean(do_bu)), 2),
-                     "bottom_up_edges_examined_per_traversed": round(do_ex / max(1, do_edges), 4),
-                     "note": "same graph, roots, parents and levels (bit-identical); phase 1 switches "
-                             "top-down/bottom-up by Beamer's rule (alpha 5, beta 1024, tuned on this graph; Beamer's CPU values are 14, 24); TEPS counts "
-                             "the same E_trav"}
+    do_edges = sum(st.traversed_edges for st in do)
+    direction_opt = {
+        "value": round(hmean([st.traversed_edges / (st.elapsed_ms * 1e-3) / 1e9 for st in do]), 3),
+        "unit": UNIT, "bfs_ms_mean": round(float(np.mean([st.elapsed_ms for st in do])), 4),
+        "bottom_up_levels_mean": round(float(np.mean([st.bottom_up_levels for st in do])), 2),
+        "bottom_up_edges_examined_per_traversed":
+            round(sum(st.edges_examined for st in do) / max(1, do_edges), 4),
+        "note": "same graph, roots, parents and levels (bit-identical); phase 1 switches "
+                "top-down/bottom-up by Beamer's rule (alpha 5, beta 1024, tuned on this graph; "
+                "Beamer's CPU values are 14, 24); TEPS counts the same E_trav"}
 
-    # e2e: the public API call (engine.run) with host-resident results
+    # e2e: the public API call (engine.run) with host-resident results, every
+    # root once; the reference's contract returns levels only
     p1 = graphs.Partition(1, [0, g.num_vertices])
-    e2e = []
-    n_e2e = min(args.e2e_steps, K)
-    h2d = 8  # the root id crosses to the device; the graph is resident
-    d2h = 0  # DistanceArray.d: levels packed to 4/8 bits on device, widened on host
-    ecfg = engine.EngineConfig(fanout=1)  # the reference's contract: levels only
-    engine.run(g, p1, int(roots[0]), ecfg)  # untimed: engine setup for this config
-    for i in range(n_e2e):
-        r = int(roots[i % len(roots)])
+    ecfg = engine.EngineConfig(fanout=1)
+    engine.run(g, p1, roots[0], ecfg)  # untimed: engine setup for this config
+    e2e, d2h, gpu_sha = [], 0, {}
+    for r in roots:
         t = time.perf_counter()
         d, st = engine.run(g, p1, r, ecfg)
         dt = time.perf_counter() - t
         e2e.append(st.traversed_edges / dt / 1e9)
         d2h = max(d2h, levels_readout_bytes(g.num_vertices, st.levels))
+        if len(gpu_sha) < args.cpu_roots:
+            gpu_sha[r] = sha16(d.d)
+        del d
 
-    # CPU baseline (bounded sample of the same workload, 1 thread)
-    off, adj, copy_s = host_csr(dg)
-    cpu = cpu_sample(off, adj, roots, args.cpu_budget, 2)
-    cpu_v = hmean([c[0] for c in cpu])
+    # CPU baseline: complete BFSs of the reference's CPU path on host copies
+    t = time.time()
+    off, adj = dg.csr()
+    copy_s = time.time() - t
+    cpu = cpu_baseline_leg(off, adj, roots[:args.cpu_roots], gpu_sha, copy_s)
     del off, adj
 
-    line = {
-        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1, "steps": K,
-        "warmup": W, "ms_per_step": round(bracket_ms / K, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": cfg,
-        "aggregate_gteps": round(sum(edges) / (bracket_ms * 1e-3) / 1e9, 3),
-        "bfs_ms_mean": round(float(np.mean(times)), 4),
+    line = base_line(args, cfg, 1, K, W, value, bracket_ms)
+    traffic = committed_traffic(args.scale, args.edge_factor)
+    line.update({
+        "aggregate_gteps": round(edges / (bracket_ms * 1e-3) / 1e9, 3),
+        "bfs_ms_mean": round(float(np.mean([st.elapsed_ms for st in td])), 4),
+        "bfs_per_step": len(roots),
         "graph": {"num_vertices": g.num_vertices, "num_edges": g.num_edges,
                   "build_s": round(build_s, 2), "max_degree": dg.max_degree},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "k_expand (phase 1 top-down expansion)",
-                     "achieved_def": "sum over levels of (4 B x edges + 20 B x frontier "
-                                     "vertices) / sum of k_expand event time",
+                     "frac": round(achieved / peak, 4),
+                     "traffic": traffic.get("dram_bytes_per_launch") if isinstance(traffic, dict)
+                     else traffic,
+                     "kernel": "k_expand_w (phase 1 top-down expansion)",
+                     "achieved_def": f"sum over BFSs and levels of ({BYTES_PER_EDGE} B x edges + "
+                                     f"{BYTES_PER_VERTEX} B x frontier vertices) / sum of "
+                                     "k_expand_w event time (CUDA events on the engine stream)",
                      "peak_src": peak_src,
-                     "expand_share": round(exp_ms / sum(times), 4),
-                     "expand_launches_per_bfs": exp_launch / K,
-                     "l2_probe": {"achieved": round(probe_achieved / 1e9, 2),
+                     "expand_share": round(exp_ms / sum(st.elapsed_ms for st in td), 4),
+                     "expand_launches_per_bfs": round(exp_launch / len(td), 2),
+                     "l2_probe": {"achieved": round(edges / (exp_ms * 1e-3) / 1e9, 2),
                                   "peak": round(probe_peak / 1e9, 2), "unit": "Gprobe/s",
-                                  "frac": round(probe_achieved / probe_peak, 4),
+                                  "frac": round(edges / (exp_ms * 1e-3) / probe_peak, 4),
                                   "def": "one random 4 B visited-bitmap load per traversed "
-                                         "edge / k_expand time, vs random 4 B loads over a "
+                                         "edge / k_expand_w time, vs random 4 B loads over a "
                                          "bitmap-sized (n/8 B) buffer, measured in this run "
                                          "(csrc/probe_peak.cu)"}},
-        "cpu_baseline": {"value": round(cpu_v, 5), "unit": UNIT, "cores": cpu_threads(),
-                         "kind": "port",
-                         "sample": f"oracle/bfs_omp.c top-down BFS (C + OpenMP, {cpu_threads()} "
-                                   f"threads) on the same s{args.scale} CSR copied to host "
-                                   f"({copy_s:.1f} s), 2 roots x {args.cpu_budget / 2:.0f} s budget, "
-                                   f"GTEP/s = edges scanned / time",
-                         "host_threads_available": cpu_threads()},
-        "e2e": {"value": round(hmean(e2e), 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": n_e2e,
-                "path": "paper_2103_13577_b200.engine.run(g, p, root, EngineConfig()) -> DistanceArray "
-                        "in host numpy (uint32), wall clock per call; levels cross PCIe "
-                        "packed and are widened by host threads"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(hmean(e2e), 3), "unit": UNIT, "h2d_bytes_per_step": 8 * len(roots),
+                "d2h_bytes_per_step": d2h * len(roots), "bfs": len(e2e),
+                "path": "paper_2103_13577_b200.engine.run(g, p, root, EngineConfig()) -> "
+                        "DistanceArray in host numpy (uint32), wall clock per call, every root "
+                        "once; levels cross PCIe packed and are widened by host threads"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "direction_optimizing": direction_opt,
-    }
-    print(json.dumps(line), flush=True)
+    })
+    return line
 
 
-def main_rank(args, cfg):
+def main_rank(args):
     """N > 1 under torchrun: one rank per GPU, node = rank.  The s29 graph is
     built on every GPU (deterministic); each rank keeps its partition_1d rows.
-    A step = one BFS through the device-synchronised engine (bfb_rank_bfs:
-    per-round barrier and snapshot sizes through NVLink mailboxes, snapshots
-    merged in place from peer HBM); t = max over ranks of the device time from
-    root injection to termination.  Returns rank 0's JSON line."""
+    A step = one pass over the roots through the device-synchronised engine
+    (bfb_rank_bfs: per-round barrier and snapshot sizes through NVLink
+    mailboxes, snapshots merged in place from peer HBM); t = max over ranks of
+    the device time from root injection to termination.  Returns rank 0's
+    JSON line (None on the other ranks)."""
     import torch
     import torch.distributed as dist
 
@@ -349,42 +408,49 @@ def main_rank(args, cfg):
     P = comm.size
     fanout = args.fanout or min(2, P)
     parents = not args.no_parents
+    cfg = config_of(args, P, fanout, parents)
     t0 = time.time()
     g = graphs.kronecker(args.scale, args.edge_factor, 1, device=dev)
     dg = g.device
-    build_s = time.time() - t0
+    build_s = comm.allreduce(time.time() - t0, "max")
     b = dg.partition_1d(P)
-    roots = graphs.sample_roots(g, args.roots)
+    roots = [int(r) for r in graphs.sample_roots(g, args.roots)]
     eng = bdist.RankEngine(dg, b, fanout, "butterfly", parents, comm)
     dg.set_timing(True)
     K, W = args.steps, args.warmup
 
+    def passes(count, out):
+        for _ in range(count):
+            for r in roots:
+                sizes, st = eng.node.bfs(r)
+                if out is None:
+                    continue
+                tmax = comm.allreduce(float(st.elapsed_ms), "max")
+                e = int(comm.allreduce(int(st.traversed_edges)))
+                out["teps"].append(e / (tmax * 1e-3) / 1e9)
+                out["edges"] += e
+                out["t"].append(tmax)
+                out["reached"] += sum(sizes)
+                out["launches"] += int(comm.allreduce(int(st.kernel_launches)))
+                for k in ("expand", "exchange", "commit"):
+                    out[k] += comm.allreduce(float(getattr(st, k + "_ms")), "max")
+                # NVLink payload this rank pulled (queue or bitmap snapshots)
+                # over its own exchange time; the rate is max over ranks
+                out["nvl_rate"].append(comm.allreduce(
+                    float(st.exchange_bytes) / max(1e-9, float(st.exchange_ms) * 1e-3), "max"))
+                out["nvl_bytes"] += int(comm.allreduce(int(st.exchange_bytes), "max"))
+                out["bu"] += int(st.bottom_up_levels)
+                out["exp_launches"] += int(st.expand_launches)  # this rank's, one per level
+
     def timed(direction):
         dg.set_direction(direction)
-        for i in range(W):
-            eng.node.bfs(int(roots[(K + i) % len(roots)]))
+        passes(W if direction == "top-down" else 1, None)
         comm.barrier()
-        out = {"teps": [], "edges": [], "t": [], "launches": 0, "expand": 0.0, "exchange": 0.0,
-               "commit": 0.0, "bu": 0, "reached": 0, "nvl_rate": [], "nvl_bytes": 0}
+        out = {"teps": [], "edges": 0, "t": [], "launches": 0, "expand": 0.0, "exchange": 0.0,
+               "commit": 0.0, "bu": 0, "reached": 0, "nvl_rate": [], "nvl_bytes": 0,
+               "exp_launches": 0}
         dg.timer_start()
-        for i in range(K):
-            sizes, st = eng.node.bfs(int(roots[i % len(roots)]))
-            tmax = comm.allreduce(float(st.elapsed_ms), "max")
-            e = int(comm.allreduce(int(st.traversed_edges)))
-            out["teps"].append(e / (tmax * 1e-3) / 1e9)
-            out["edges"].append(e)
-            out["t"].append(tmax)
-            out["launches"] += int(st.kernel_launches)
-            out["expand"] += comm.allreduce(float(st.expand_ms), "max")
-            out["exchange"] += comm.allreduce(float(st.exchange_ms), "max")
-            # NVLink payload this rank pulled (queue or bitmap snapshots) and
-            # its own exchange time; the rate is max over ranks
-            out["nvl_rate"].append(comm.allreduce(
-                float(st.exchange_bytes) / max(1e-9, float(st.exchange_ms) * 1e-3), "max"))
-            out["nvl_bytes"] += int(comm.allreduce(int(st.exchange_bytes), "max"))
-            out["commit"] += comm.allreduce(float(st.commit_ms), "max")
-            out["bu"] += int(st.bottom_up_levels)
-            out["reached"] += sum(sizes)
+        passes(K, out)
         out["bracket"] = comm.allreduce(dg.timer_stop(), "max")
         return out
 
@@ -392,106 +458,127 @@ def main_rank(args, cfg):
         td = timed("top-down")
     do = timed("optimizing")
     dg.set_direction("top-down")
+    nb = len(td["t"])
     value = hmean(td["teps"])
     peak, peak_src = measured_peaks()
-    # per-rank algorithmic expand bytes (4 B/edge + 24 B per owned reached
-    # vertex, summed over ranks) over the slowest rank's expand time
-    level_bytes = 4 * sum(td["edges"]) + (24 if parents else 20) * td["reached"]
+    level_bytes = BYTES_PER_EDGE * td["edges"] + BYTES_PER_VERTEX * td["reached"]
     achieved = level_bytes / P / (td["expand"] * 1e-3) / 1e9 if td["expand"] > 0 else 0.0
 
-    # e2e: the public multi-rank API (every rank calls RankEngine.run(root) and
-    # gets the DistanceArray in host numpy); wall clock, max over ranks
-    e2e = []
-    d2h = 0
-    eng.run(int(roots[0]), parents=False)
-    for i in range(min(args.e2e_steps, K)):
-        r = int(roots[i % len(roots)])
+    # e2e: the public multi-rank API (every rank calls RankEngine.run(root)
+    # and gets the DistanceArray in host numpy); wall clock, max over ranks
+    e2e, d2h, gpu_sha = [], 0, {}
+    eng.run(roots[0], parents=False)
+    for r in roots:
         comm.barrier()
         t = time.perf_counter()
-        d, st = eng.run(r, parents=False)  # the reference's contract: levels only
+        d, st = eng.run(r, parents=False)
         dt = comm.allreduce(time.perf_counter() - t, "max")
         e2e.append(st.traversed_edges / dt / 1e9)
         d2h = max(d2h, levels_readout_bytes(g.num_vertices, st.levels))
+        if len(gpu_sha) < args.cpu_roots:
+            gpu_sha[r] = sha16(d.d)
+        del d
 
-    cfg = dict(cfg, fanout=fanout, num_parts=P)
-    line = {
-        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": P, "steps": K,
-        "warmup": W, "ms_per_step": round(td["bracket"] / K, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": cfg,
-        "aggregate_gteps": round(sum(td["edges"]) / (td["bracket"] * 1e-3) / 1e9, 3),
+    cpu = None
+    if comm.rank == 0:
+        t = time.time()
+        off, adj = dg.csr()
+        copy_s = time.time() - t
+        cpu = cpu_baseline_leg(off, adj, roots[:args.cpu_roots], gpu_sha, copy_s)
+        del off, adj
+    comm.barrier()
+
+    traffic = committed_traffic(args.scale, args.edge_factor)
+    traffic_n = None
+    if isinstance(traffic, dict) and traffic.get("algorithmic_bytes_per_launch"):
+        # DRAM bytes per launch scale with the algorithmic bytes (ncu at N = 1)
+        ratio = traffic["dram_bytes_per_launch"] / traffic["algorithmic_bytes_per_launch"]
+        traffic_n = int(ratio * level_bytes / P / max(1, td["exp_launches"]))
+    line = base_line(args, cfg, P, K, W, value, td["bracket"])
+    line.update({
+        "aggregate_gteps": round(td["edges"] / (td["bracket"] * 1e-3) / 1e9, 3),
         "bfs_ms_mean": round(float(np.mean(td["t"])), 4),
-        "phase_ms_mean_max_over_ranks": {k: round(td[k] / K, 4)
+        "bfs_per_step": len(roots),
+        "phase_ms_mean_max_over_ranks": {k: round(td[k] / nb, 4)
                                          for k in ("expand", "exchange", "commit")},
         "graph": {"num_vertices": g.num_vertices, "num_edges": g.num_edges,
                   "build_s": round(build_s, 2), "max_degree": dg.max_degree},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": traffic_n,
+                     "traffic_src": "N = 1 ncu DRAM/algorithmic byte ratio of k_expand_w "
+                                    "(profiles/expand_traffic.json) x this run's per-GPU "
+                                    "algorithmic bytes per BFS",
                      "kernel": "k_expand_w (phase 1 top-down expansion), per GPU",
-                     "achieved_def": "(4 B x edges + 24 B x reached vertices) / N per GPU / "
-                                     "slowest rank's expand time",
+                     "achieved_def": f"({BYTES_PER_EDGE} B x edges + {BYTES_PER_VERTEX} B x "
+                                     "reached vertices) / N per GPU / slowest rank's expand time",
                      "peak_src": peak_src},
-        "cpu_baseline": None,
-        "e2e": {"value": round(hmean(e2e), 3), "unit": UNIT, "h2d_bytes_per_step": 8 * P,
-                "d2h_bytes_per_step": d2h * P, "steps": len(e2e),
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(hmean(e2e), 3), "unit": UNIT, "h2d_bytes_per_step": 8 * P * len(roots),
+                "d2h_bytes_per_step": d2h * P * len(roots), "bfs": len(e2e),
                 "path": "paper_2103_13577_b200.dist.RankEngine.run(root) on every rank -> "
-                        "DistanceArray in host numpy, wall clock max over ranks"},
+                        "DistanceArray in host numpy, wall clock max over ranks, every root once"},
         "gpu_launches": td["launches"],
         "clocks": clk.summary(),
         "exchange": "device-synchronised butterfly: per round publish -> NVLink mailbox signal "
-                    "-> spin-wait -> in-place merge of the sources' snapshot bitmaps (CUDA IPC)",
+                    "-> spin-wait -> in-place merge of the sources' snapshots (CUDA IPC)",
         "roofline_nvlink": {"bound": "nvlink", "unit": "GB/s", "peak": 900.0,
                             "achieved": round(float(np.mean(td["nvl_rate"])) / 1e9, 1),
                             "frac": round(float(np.mean(td["nvl_rate"])) / 900e9, 4),
-                            "bytes_per_bfs_max_rank": td["nvl_bytes"] // K,
+                            "bytes_per_bfs_max_rank": td["nvl_bytes"] // nb,
                             "def": "per rank: snapshot bytes pulled from peers (4 B per queued "
                                    "vertex or n/8 B per bitmap) / that rank's phase-2 time "
                                    "(publish + barrier + merge), max over ranks, mean over "
-                                   "BFS; peak = NVLink 5 per direction per GPU (nominal)"},
+                                   "BFSs; peak = NVLink 5 per direction per GPU (nominal)"},
         "direction_optimizing": {"value": round(hmean(do["teps"]), 3), "unit": UNIT,
                                  "bfs_ms_mean": round(float(np.mean(do["t"])), 4),
-                                 "bottom_up_levels_mean_per_rank": round(do["bu"] / K, 2)},
-    }
+                                 "bottom_up_levels_mean_per_rank": round(do["bu"] / nb, 2)},
+    })
+    if os.environ.get("BFB_SHARED_GPU") == "1":
+        line["note"] = "protocol run: all ranks share one GPU (BFB_SHARED_GPU=1); not a scaling number"
     return line if comm.rank == 0 else None
 
 
-def run_reference(args, cfg, n_gpus):
-    """Reference arm: the reference's CPU path (oracle port of SPEC.md's BFS)
-    on the host cores, bounded samples per step; rank 0 only."""
+def run_reference(args, n_gpus):
+    """Reference arm: the reference's CPU path (oracle port of SPEC.md's BFS,
+    C + OpenMP on every host thread); each step one COMPLETE BFS from the next
+    root; rank 0 only.  The input graph is built on device outside the timed
+    region (the reference's numpy build cannot make s29 on a host) and copied
+    to host."""
     from paper_2103_13577_b200 import graphs
 
     t0 = time.time()
     g = graphs.kronecker(args.scale, args.edge_factor, 1)
-    roots = graphs.sample_roots(g, args.roots)
-    off, adj, copy_s = host_csr(g.device)
+    roots = [int(r) for r in graphs.sample_roots(g, args.roots)]
+    t = time.time()
+    off, adj = g.device.csr()
+    copy_s = time.time() - t
     g.device.close()
     build_s = time.time() - t0
     K, W = args.steps, args.warmup
-    budget = min(args.cpu_budget, 150.0) / max(1, K + W)  # whole run within a few minutes
-    cpu_sample(off, adj, roots[K:K + W] if len(roots) > K else roots, budget * W, W)
+    for i in range(W):
+        cpu_complete_bfs(off, adj, roots[(K + i) % len(roots)])
     t = time.perf_counter()
-    res = cpu_sample(off, adj, roots, budget * K, K)
+    res = [cpu_complete_bfs(off, adj, roots[i % len(roots)]) for i in range(K)]
     wall = time.perf_counter() - t
-    value = hmean([r[0] for r in res])
-    line = {
-        "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": n_gpus, "steps": K,
-        "warmup": W, "ms_per_step": round(wall * 1e3 / K, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "impl": "reference", "config": cfg,
+    value = hmean([r[1] for r in res])
+    cfg = config_of(args, n_gpus, args.fanout or min(2, n_gpus), not args.no_parents)
+    cfg["roots_timed"] = min(K, len(roots))
+    line = base_line(args, cfg, n_gpus, K, W, value, wall * 1e3)
+    sample = (f"each step: one complete top-down BFS from the next root by oracle/bfs_omp.c "
+              f"(C + OpenMP restatement of SPEC.md:136-163, {cpu_threads()} threads); input graph "
+              f"(generator, symmetrize, CSR) built on device outside the timed region and copied "
+              f"to host ({build_s:.1f} s incl. {copy_s:.1f} s copy)")
+    line.update({
+        "impl": "reference",
         "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": cpu_threads(),
-                         "kind": "port",
-                         "sample": f"each step: oracle/bfs_omp.c top-down BFS (C + OpenMP "
-                                   f"restatement of SPEC.md:136-163, {cpu_threads()} threads) from "
-                                   f"the next root, stopped after {budget:.2f} s; input graph "
-                                   f"(generator, symmetrize, CSR) built on device outside the "
-                                   f"timed region and copied to host "
-                                   f"({build_s:.1f} s incl. {copy_s:.1f} s copy)",
+                         "kind": "port", "sample": sample,
                          "host_threads_available": cpu_threads()},
         "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-    }
+    })
+    line["ms_per_step"] = round(wall * 1e3 / K, 3)
     print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

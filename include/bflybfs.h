@@ -65,6 +65,10 @@ typedef struct bfb_run_stats {
   double expand_max_part_ms;         /* timing mode, CN > 1 in one context: sum over
                                         levels of the slowest node's phase 1 (the
                                         critical path if each node had its own GPU) */
+  int64_t switch_checksum;           /* direction-optimizing: sum over levels of
+                                        (level + 1) x the next frontier's degree sum
+                                        that fed Beamer's rule -- equal on every node
+                                        (rank mode) and to the one-context run */
 } bfb_run_stats;
 
 /* Outcome of bfb_parse_text (graphs.py:96-202 ParseError carries the line). */
@@ -203,6 +207,12 @@ int bfb_copy_parents(bfb_ctx* ctx, int64_t* parents_out);
  * parents: *errors_out = bitmask (1 root, 2 reachability mismatch on an edge,
  * 4 edge spans >1 level, 8 reached vertex without predecessor, 16 bad parent). */
 int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out);
+/* The same certificate for caller-supplied results (host arrays: n uint32
+ * levels, and n int64 parents with -1 = none, or NULL): checks any levels /
+ * parents against the resident graph -- the verify command's device check
+ * and the certificate's own negative tests.  Allocates its device copies. */
+int bfb_validate_host(bfb_ctx* ctx, int64_t root, const uint32_t* levels, const int64_t* parents,
+                      int64_t* errors_out);
 
 /* Measurement helper (bench.py roofline, not part of the reference API): the
  * random-probe ceiling of phase 1 -- random 4-byte loads over a `bytes`-sized

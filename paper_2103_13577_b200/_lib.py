@@ -48,6 +48,7 @@ class RunStatsC(ctypes.Structure):
         ("edges_examined", c_int64),
         ("bottom_up_levels", c_int64),
         ("expand_max_part_ms", c_double),
+        ("switch_checksum", c_int64),
     ]
 
 
@@ -103,6 +104,7 @@ _SIGNATURES = {
     "bfb_copy_levels": (c_int, [c_void_p, _U32P]),
     "bfb_copy_parents": (c_int, [c_void_p, _I64P]),
     "bfb_validate": (c_int, [c_void_p, c_int64, _I64P]),
+    "bfb_validate_host": (c_int, [c_void_p, c_int64, _U32P, _I64P, _I64P]),
     "bfb_probe_peak": (c_int, [c_void_p, c_int64, _I64P, POINTER(c_double)]),
     "bfb_parse_text": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int64, c_int64,
                                c_int64, POINTER(ParseResultC)]),

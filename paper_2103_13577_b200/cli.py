@@ -10,10 +10,11 @@ all vertices with ``seed``, one engine run per root, runs sorted b
 time with ``trim`` fastest and slowest dropped, trimmed mean time, teps_nominal
 = |E| / mean and teps_touched = traversed edges / mean, JSON on
 stdout and optional per-run CSV.  verify runs
-the CN-node engine and the single-node engine (the bfs_top_down degenerate
-case) per root and compares full distance arrays, plus the device
-certificate of SPEC.md:130-132; exit status 1 with (root, vertex, expected,
-got) on the first mismatch.
+the CN-node engine per root and compares its full distance array with an
+independent host BFS over the graph's host CSR (``_host_bfs``, the SPEC's
+bfs_top_down, SPEC.md:136-163 -- no device code shared with the engine), and
+always requires the device certificate of SPEC.md:130-132 as well; exit
+status 1 with (root, vertex, expected, got) on the first mismatch.
 """
 
 from __future__ import annotations
@@ -89,23 +90,45 @@ def cmd_bench(args):
     return 0
 
 
+def _host_bfs(offsets, adjacency, root):
+    """verify's reference (SPEC.md:136-163 bfs_top_down): level-synchronous
+    BFS on the host CSR in numpy, frontier expanded a level at a time.  It is
+    the checker of the verify command, never a path that produces results."""
+    n = offsets.size - 1
+    d = np.full(n, graphs.UNREACHED, dtype=np.uint32)
+    d[root] = 0
+    frontier = np.array([root], dtype=np.int64)
+    level = 0
+    while frontier.size:
+        starts, ends = offsets[frontier], offsets[frontier + 1]
+        cnt = ends - starts
+        idx = np.repeat(starts - np.concatenate(([0], np.cumsum(cnt)[:-1])), cnt) + \
+            np.arange(int(cnt.sum()), dtype=np.int64)
+        nb = np.unique(adjacency[idx])
+        nb = nb[d[nb] == graphs.UNREACHED]
+        level += 1
+        d[nb] = level
+        frontier = nb.astype(np.int64)
+    return d
+
+
 def cmd_verify(args):
     g, _ = _load_graph(args)
     p = graphs.partition_1d(g, args.nodes)
-    p1 = graphs.partition_1d(g, 1)
     roots, _ = sample_roots(g.num_vertices, args.roots, args.seed)
     cfg = engine.EngineConfig(fanout=args.fanout, strategy=args.strategy)
+    off, adj = np.asarray(g.offsets), np.asarray(g.adjacency)
     for r in roots:
         r = int(r)
-        ref, _ = engine.run(g, p1, r)
+        ref = _host_bfs(off, adj, r)
         got, _ = engine.run(g, p, r, cfg)
-        bad = np.flatnonzero(ref.d != got.d)
+        bad = np.flatnonzero(ref != got.d)
         if bad.size:
             v = int(bad[0])
-            print(json.dumps({"ok": False, "root": r, "vertex": v, "expected": int(ref.d[v]),
+            print(json.dumps({"ok": False, "root": r, "vertex": v, "expected": int(ref[v]),
                               "got": int(got.d[v])}))
             return 1
-        cert = g.device.validate(r) if getattr(g, "device", None) is not None else 0
+        cert = graphs.device_graph(g).validate(r)
         if cert:
             print(json.dumps({"ok": False, "root": r, "certificate_errors": int(cert)}))
             return 1

@@ -296,6 +296,8 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
 int engine_copy_levels(bfb_ctx* ctx, uint32_t* out);
 int engine_copy_parents(bfb_ctx* ctx, int64_t* out);
 int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs);
+int validate_host(bfb_ctx* ctx, int64_t root, const uint32_t* levels, const int64_t* parents,
+                  int64_t* errs);
 int probe_peak(bfb_ctx* ctx, int64_t bytes, int64_t* probes_out, double* ms_out);
 void engine_release(bfb_ctx* ctx);
 

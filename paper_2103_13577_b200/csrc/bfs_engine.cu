@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t fr = 0;
+  int64_t fr = 0, re = 0;
   // with the parent pass a unit's work varies with its new vertices: units
   // are handed out in chunks from a counter (zeroed by k_commit_prep)
   int64_t unit = kParents ? grab_units(v.ctr, lane) : gw;
@@ -619,6 +619,12 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
     const uint32_t c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(own));
     int64_t d = 0;
     if (c) d = warp_sum_i64(word_degree_sum16(own, v.abase + unit * 32 + lane, v.deg16, off));
+    // rank mode, direction-optimizing: the new vertices of the partial
+    // boundary words that a neighbouring node owns are in neither this
+    // node's q_edges nor k_commit_rest's words -- sum them here so every
+    // rank's next-frontier degree sum is the same global number
+    if (v.rest_degrees && !v.rebuild && (nb & ~own))
+      re += word_degree_sum16(nb & ~own, v.abase + unit * 32 + lane, v.deg16, off);
     if (lane == 0) {
       v.ucnt[unit] = c;
       v.udeg[unit] = d;
@@ -687,6 +693,11 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
   __shared__ int64_t red[32];
   fr = block_sum_i64(fr, red);
   if (threadIdx.x == 0 && fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
+  if (v.rest_degrees) {
+    re = block_sum_i64(re, red);
+    if (threadIdx.x == 0 && re)
+      atomicAdd((unsigned long long*)&v.ctr->rest_edges, (unsigned long long)re);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_unit_scan_reduce(PartView v) {
@@ -926,7 +937,7 @@ __global__ void __launch_bounds__(256) k_commit_light_count(PartView v, const in
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t fr = 0, qc = 0, qe = 0;
+  int64_t fr = 0, qc = 0, qe = 0, re = 0;
   for (int64_t unit = gw; unit < v.nunits; unit += nw) {
     uint32_t a, nb, own;
     unit_word(v, unit, lane, a, nb, own);
@@ -949,11 +960,17 @@ __global__ void __launch_bounds__(256) k_commit_light_count(PartView v, const in
       qc += __popc(own);
       qe += word_degree_sum16(own, w0 + lane, v.deg16, off);
     }
+    if (v.rest_degrees && (nb & ~own)) re += word_degree_sum16(nb & ~own, w0 + lane, v.deg16, off);
   }
   __shared__ int64_t red[32];
   fr = block_sum_i64(fr, red);
   qc = block_sum_i64(qc, red);
   qe = block_sum_i64(qe, red);
+  if (v.rest_degrees) {
+    re = block_sum_i64(re, red);
+    if (threadIdx.x == 0 && re)
+      atomicAdd((unsigned long long*)&v.ctr->rest_edges, (unsigned long long)re);
+  }
   if (threadIdx.x == 0) {
     if (fr) atomicAdd((unsigned long long*)&v.ctr->frontier, (unsigned long long)fr);
     if (qc) atomicAdd((unsigned long long*)&v.ctr->q_count, (unsigned long long)qc);
@@ -1500,6 +1517,8 @@ struct EngineTables {
   }
 };
 
+bool rank_mode(const bfb_ctx* ctx) { return ctx->tables && ctx->tables->rank >= 0; }
+
 void engine_release(bfb_ctx* ctx) {
   ctx->parts.clear();
   ctx->run.release();
@@ -1698,6 +1717,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   nsizes = 1;
   ctx->last_sizes.assign(1, 1);
   int64_t reached = 1;
+  int64_t switch_chk = 0;
   const unsigned small_grid = grid_cap(nwords, 256, sms, 4);
   while (true) {
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
@@ -1802,6 +1822,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       frontier = ctx->pinned[0];
       int64_t mf = 0;
       for (int g = 0; g < P; ++g) mf += ctx->pinned[2 + g];
+      switch_chk += (level + 1) * mf;
       const double mu = (double)(ctx->g.m - ctx->pinned[1]);  // unexplored edges
       next_bu = bottom_up;
       if (!bottom_up && (double)mf > mu / ctx->do_alpha && frontier > prev_frontier)
@@ -1910,6 +1931,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     st->edges_examined = rc.edges_examined;
     st->bottom_up_levels = bu_levels;
     st->expand_max_part_ms = t_expand_max;
+    st->switch_checksum = switch_chk;
   }
   // buffer-bound check: incoming <= f * |V|
   for (auto x : hw)
@@ -1962,6 +1984,41 @@ int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs) {
   unsigned h = 0;
   BFB_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *errs = (int64_t)h;
+  return BFB_OK;
+}
+
+__global__ void k_parents_from_i64(const int64_t* __restrict__ in, uint32_t* __restrict__ out,
+                                   int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = in[i];
+    out[i] = (p < 0 || p >= (int64_t)kNone) ? kNone : (uint32_t)p;
+  }
+}
+
+int validate_host(bfb_ctx* ctx, int64_t root, const uint32_t* levels, const int64_t* parents,
+                  int64_t* errs) {
+  const int64_t n = ctx->g.n;
+  cudaStream_t s = ctx->stream;
+  DevBuf<uint32_t> lv, par;
+  DevBuf<int64_t> par64;
+  DevBuf<unsigned> err;
+  BFB_TRY(lv.alloc(n));
+  BFB_TRY(err.alloc(1));
+  BFB_CUDA(cudaMemcpyAsync(lv.p, levels, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  if (parents) {
+    BFB_TRY(par64.alloc(n));
+    BFB_TRY(par.alloc(n));
+    BFB_CUDA(cudaMemcpyAsync(par64.p, parents, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k_parents_from_i64<<<grid_cap(n, 256, ctx->num_sms, 8), 256, 0, s>>>(par64.p, par.p, n);
+  }
+  BFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(unsigned), s));
+  k_validate<<<grid_cap(n * 32, 256, ctx->num_sms, 16), 256, 0, s>>>(
+      ctx->g.offsets.p, ctx->g.adj.p, n, lv.p, parents ? par.p : nullptr, root, err.p);
+  unsigned h = 0;
+  BFB_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  BFB_CUDA(cudaStreamSynchronize(s));
   *errs = (int64_t)h;
   return BFB_OK;
 }
@@ -2081,6 +2138,7 @@ int rank_begin(bfb_ctx* ctx, int64_t root) {
   const int64_t nwords = (n + 31) / 32;
   BFB_CUDA(cudaEventRecord(D->ev[0], s));
   BFB_CUDA(cudaMemsetAsync(ctx->run.p, 0, sizeof(RunCounters), s));
+  BFB_CUDA(cudaMemsetAsync(D->err.p, 0, sizeof(int32_t), s));  // a past barrier timeout
   BFB_CUDA(cudaMemsetAsync(p.visited.p, 0, nwords * sizeof(uint32_t), s));
   BFB_CUDA(cudaMemsetAsync(p.start.p, 0, nwords * sizeof(uint32_t), s));
   if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
@@ -2436,6 +2494,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   bool bottom_up = ctx->direction == 2;
   int64_t bu_levels = 0, prev_frontier = 1, nsizes = 1, launches = 0;
   int64_t seen_edges = 0;  // degree sum of every frontier so far (direction switch)
+  int64_t switch_chk = 0;
   if (ctx->direction == 1) {
     int64_t ob[2];
     BFB_CUDA(cudaMemcpy(ob, off + root, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -2519,14 +2578,17 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       // Beamer's rule on global quantities, so every node takes the same
       // direction: an edge (u on node g, v on node h) is traversed only if g
       // runs top-down or h bottom-up, so mixed directions would lose edges.
-      // The next frontier's degree sum = owned part (count pass) + the rest
-      // (k_commit_rest), identical on all nodes, as is the running sum.
+      // The next frontier's degree sum = owned part (count pass) + the
+      // non-owned rest: the words outside [wlo, whi) (k_commit_rest) and the
+      // neighbours' bits of the partial boundary words (count pass), so the
+      // sum -- and the running sum -- is the same global number on all nodes.
       BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 3, &p.ctr.p->rest_edges, sizeof(int64_t),
                                cudaMemcpyDeviceToHost, s));
       BFB_CUDA(cudaStreamSynchronize(s));
       const int64_t frontier = ctx->pinned[2], mf = ctx->pinned[1] + ctx->pinned[3];
       seen_edges += mf;
+      switch_chk += (D->level + 1) * mf;
       const double mu = (double)(ctx->g.m - seen_edges);
       next_bu = bottom_up;
       if (!bottom_up && (double)mf > mu / ctx->do_alpha && frontier > prev_frontier)
@@ -2587,6 +2649,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     st->exchange_ms = t_exchange;
     st->commit_ms = t_commit;
     st->expand_launches = expand_launches;
+    st->switch_checksum = switch_chk;
   }
   if (hw > (int64_t)ctx->fanout * n && ctx->strategy == BFB_STRATEGY_BUTTERFLY)
     return fail(BFB_ERR_CAPACITY, "buffer bound violated");

@@ -80,6 +80,17 @@ using namespace bfb;
 #define NEED_GRAPH(ctx) \
   if (!(ctx)->g.valid) return fail(BFB_ERR_STATE, "no graph loaded")
 
+// The single-context entry points (bfb_bfs and its read-outs) index every
+// node's buffers; after bfb_rank_setup the context holds one node only.
+namespace bfb {
+bool rank_mode(const bfb_ctx* ctx);
+}
+#define NOT_RANK_MODE(ctx)                                                      \
+  if (bfb::rank_mode(ctx))                                                      \
+  return fail(BFB_ERR_STATE, "context is in multi-process (rank) mode: use bfb_rank_*")
+#define NEED_RANK_MODE(ctx) \
+  if (!bfb::rank_mode(ctx)) return fail(BFB_ERR_STATE, "not in rank mode (bfb_rank_setup first)")
+
 extern "C" {
 
 const char* bfb_version(void) { return "bflybfs-b200 0.1 (sm_100a)"; }
@@ -316,6 +327,7 @@ int bfb_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_o
             int64_t* frontier_sizes_out, int64_t max_levels, int64_t* buffer_high_water_out,
             bfb_run_stats* stats_out) {
   CTX_GUARD(ctx);
+  NOT_RANK_MODE(ctx);
   NEED_GRAPH(ctx);
   return engine_bfs(ctx, root, levels_out, parents_out, frontier_sizes_out, max_levels,
                     buffer_high_water_out, stats_out);
@@ -336,12 +348,23 @@ int bfb_copy_levels(bfb_ctx* ctx, uint32_t* levels_out) {
 
 int bfb_copy_parents(bfb_ctx* ctx, int64_t* parents_out) {
   CTX_GUARD(ctx);
+  NOT_RANK_MODE(ctx);
   return engine_copy_parents(ctx, parents_out);
 }
 
 int bfb_validate(bfb_ctx* ctx, int64_t root, int64_t* errors_out) {
   CTX_GUARD(ctx);
+  NOT_RANK_MODE(ctx);
   return engine_validate(ctx, root, errors_out);
+}
+
+int bfb_validate_host(bfb_ctx* ctx, int64_t root, const uint32_t* levels, const int64_t* parents,
+                      int64_t* errors_out) {
+  CTX_GUARD(ctx);
+  NEED_GRAPH(ctx);
+  if (!levels || !errors_out) return fail(BFB_ERR_INVALID, "null argument");
+  if (root < 0 || root >= ctx->g.n) return fail(BFB_ERR_ROOT, "root out of range");
+  return validate_host(ctx, root, levels, parents, errors_out);
 }
 
 int bfb_parse_text(bfb_ctx* ctx, const char* data, int64_t len, int fmt, int newline,
@@ -401,28 +424,33 @@ int bfb_rank_setup(bfb_ctx* ctx, int num_parts, const int64_t* boundaries, int f
 
 int bfb_rank_ipc_handles(bfb_ctx* ctx, void* handles_out) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (!handles_out) return fail(BFB_ERR_INVALID, "null output");
   return rank_ipc_handles(ctx, handles_out);
 }
 
 int bfb_rank_open_peer(bfb_ctx* ctx, int peer, const void* handles) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (!handles) return fail(BFB_ERR_INVALID, "null handles");
   return rank_open_peer(ctx, peer, handles);
 }
 
 int bfb_rank_begin(bfb_ctx* ctx, int64_t root) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   return rank_begin(ctx, root);
 }
 
 int bfb_rank_expand(bfb_ctx* ctx) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   return rank_expand(ctx);
 }
 
 int bfb_rank_publish(bfb_ctx* ctx, int parity, int64_t* count_out) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (!count_out || (parity != 0 && parity != 1)) return fail(BFB_ERR_INVALID, "bad argument");
   return rank_publish(ctx, parity, count_out);
 }
@@ -430,6 +458,7 @@ int bfb_rank_publish(bfb_ctx* ctx, int parity, int64_t* count_out) {
 int bfb_rank_merge(bfb_ctx* ctx, int parity, const int32_t* sources, const int64_t* counts,
                    int num_sources) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (num_sources < 0 || (num_sources && (!sources || !counts)) || (parity != 0 && parity != 1))
     return fail(BFB_ERR_INVALID, "bad argument");
   return rank_merge(ctx, parity, sources, counts, num_sources);
@@ -437,30 +466,35 @@ int bfb_rank_merge(bfb_ctx* ctx, int parity, const int32_t* sources, const int64
 
 int bfb_rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (!frontier_out || !owned_out) return fail(BFB_ERR_INVALID, "null output");
   return rank_commit(ctx, frontier_out, owned_out);
 }
 
 int bfb_rank_finish(bfb_ctx* ctx, bfb_run_stats* stats_out) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   return rank_finish(ctx, stats_out);
 }
 
 int bfb_rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
                  bfb_run_stats* stats_out) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (max_levels < 0) return fail(BFB_ERR_INVALID, "bad argument");
   return rank_bfs(ctx, root, sizes_out, max_levels, stats_out);
 }
 
 int bfb_rank_parents(bfb_ctx* ctx, int64_t* parents_out) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (!parents_out) return fail(BFB_ERR_INVALID, "null output");
   return rank_parents(ctx, parents_out);
 }
 
 int bfb_rank_parents_raw(bfb_ctx* ctx, uint32_t* parents_out) {
   CTX_GUARD(ctx);
+  NEED_RANK_MODE(ctx);
   if (!parents_out) return fail(BFB_ERR_INVALID, "null output");
   return rank_parents_raw(ctx, parents_out);
 }

@@ -271,3 +271,17 @@ class DeviceGraph:
         e = c_int64()
         check(_lib.load().bfb_validate(self.handle, int(root), byref(e)))
         return e.value
+
+    def validate_levels(self, root, levels, parents=None):
+        """The same certificate for given levels (uint32[n]) and optional
+        parents (int64[n], -1 = none): bitmask, 0 = valid (1 root, 2 edge with
+        one endpoint unreached, 4 edge spanning > 1 level, 8 reached vertex
+        without a predecessor, 16 bad parent)."""
+        lv = np.ascontiguousarray(levels, dtype=np.uint32)
+        pa = None if parents is None else np.ascontiguousarray(parents, dtype=np.int64)
+        if lv.size != self._n or (pa is not None and pa.size != self._n):
+            raise ValueError("levels / parents must have num_vertices entries")
+        e = c_int64()
+        check(_lib.load().bfb_validate_host(self.handle, int(root), ptr(lv, ctypes.c_uint32),
+                                            ptr(pa, ctypes.c_int64), byref(e)))
+        return e.value

@@ -181,6 +181,8 @@ class GpuNode:
                                        max_levels, byref(st)))
         if st.levels > max_levels:
             raise RuntimeError("more levels than max_levels")
+        self.last_bottom_up_levels = int(st.bottom_up_levels)
+        self.last_switch_checksum = int(st.switch_checksum)
         return sizes[:st.levels].tolist(), st
 
     def finish(self):

@@ -45,3 +45,30 @@ def reference_graphs():
     from bflybfs import graphs
 
     return graphs
+
+
+@pytest.fixture(scope="session")
+def reference_objects():
+    """Reference Graph / Partition objects for the drop-in tests, never
+    skipped: the live reference's own objects where /root/reference exists,
+    otherwise foreign stand-in objects (tests/ref_types.py) over arrays the
+    reference produced (tests/golden/ref_objects.npz).  Returns a loader
+    name -> (Graph, Partition, {root: levels}, source)."""
+    from tests import ref_types
+
+    def load(name):
+        g, p, levels = ref_types.load(name)
+        if os.path.isdir(REF_SRC):
+            if REF_SRC not in sys.path:
+                sys.path.insert(0, REF_SRC)
+            from bflybfs import graphs as R
+
+            s, ef, seed = {"s12_ef8_seed3": (12, 8, 3), "s10_ef8_seed1": (10, 8, 1)}[name]
+            rg = R.build_csr(R.symmetrize(R.generate_rmat(s, ef, seed)))
+            rp = R.partition_1d(rg, p.num_parts)
+            assert np.array_equal(rg.offsets, g.offsets) and np.array_equal(rg.adjacency, g.adjacency)
+            assert np.array_equal(rp.boundaries, p.boundaries)
+            return rg, rp, levels, "live reference"
+        return g, p, levels, "reference arrays (fixture)"
+
+    return load

@@ -186,12 +186,21 @@ def test_isolated_root_and_determinism():
     assert np.array_equal(a.d, b.d)
 
 
-def test_reference_graph_objects(reference_graphs):
-    R = reference_graphs
-    rg = R.build_csr(R.symmetrize(R.generate_rmat(12, 8, 3)))
-    rp = R.partition_1d(rg, 3)
-    d, st = engine.run(rg, rp, 5, engine.EngineConfig(fanout=2))
-    assert np.array_equal(d.d, ob.bfs_top_down(rg.offsets, rg.adjacency, 5))
+def test_reference_graph_objects(reference_objects):
+    """The drop-in (SURVEY §8 b): engine.run on the reference's Graph /
+    Partition objects (graphs.py:53-93), 3 nodes, fanout 2; levels equal the
+    independent scipy BFS of the fixture and the oracle."""
+    rg, rp, levels, _ = reference_objects("s12_ef8_seed3")
+    for r, want in levels.items():
+        for cfg in (engine.EngineConfig(fanout=2, parents=True),
+                    engine.EngineConfig(fanout=1, strategy="all2all"),
+                    engine.EngineConfig(fanout=3, direction="optimizing")):
+            d, st = engine.run(rg, rp, r, cfg)
+            assert np.array_equal(d.d, want), (r, cfg)
+            assert np.array_equal(d.d, ob.bfs_top_down(rg.offsets, rg.adjacency, r))
+            assert st.per_level_frontier_size == ob.level_sizes(want)
+            if cfg.parents:
+                assert not ov.check_parents(rg.offsets, rg.adjacency, r, d.d, d.parents)
 
 
 @pytest.mark.slow
@@ -237,8 +246,8 @@ def test_scale24_golden(golden):
 
 @pytest.mark.slow
 def test_config3_s27_ef16_butterfly_parts():
-    """BASELINE config 3 at full size (Kronecker s27 ef16, fanout 2) with 2
-    and 4 butterfly nodes as parts of one GPU: levels identical to the
+    """BASELINE config 3 at full size (Kronecker s27 ef16, fanout 2) with 2,
+    4 and 8 butterfly nodes as parts of one GPU: levels identical to the
     single-node run, device certificate, rounds = levels x ceil(log2 CN), and
     the per-round incoming snapshot within the f * |V| bound."""
     g = graphs.kronecker(27, 16, 1)
@@ -249,12 +258,12 @@ def test_config3_s27_ef16_butterfly_parts():
     assert dg.validate(r) == 0
     want = sha16(ref)
     del ref
-    for cn in (2, 4):
+    for cn in (2, 4, 8):
         dg.setup(dg.partition_1d(cn), 2, "butterfly", parents=True)
         lv, _, s2, st, hw = dg.bfs(r)
         assert sha16(lv) == want and s2 == sizes
         assert dg.validate(r) == 0
-        assert st.rounds_executed == len(sizes) * {2: 1, 4: 2}[cn]
+        assert st.rounds_executed == len(sizes) * {2: 1, 4: 2, 8: 3}[cn]
         assert max(hw) <= 2 * g.num_vertices
 
 

@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cases, out_dir):
+def _worker(rank, world, port, cases, out_dir, scale=14):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -39,7 +39,7 @@ def _worker(rank, world, port, cases, out_dir):
     from paper_2103_13577_b200 import graphs
 
     comm = bd.Comm()
-    g = graphs.kronecker(14, 8, 1, device=0)
+    g = graphs.kronecker(scale, 8, 1, device=0)
     dg = g.device
     b = dg.partition_1d(world)
     results = []
@@ -91,3 +91,80 @@ def test_ipc_ranks_on_one_gpu(world):
                     assert res["rm"] == ost.remote_messages
                     assert res["rv"] == ost.remote_vertices_transferred
                     assert res["hw"] == ost.buffer_high_water
+
+
+def test_ipc_ranks_s20_golden(golden):
+    """The device-synchronised rank path (one process per node, peers' HBM
+    over CUDA IPC) on the s20 golden graph: 2 ranks, fanout 2, top-down and
+    direction-optimizing; levels against the golden sha (reference graphs.py
+    + scipy BFS), sizes and traversed edges against the golden entry."""
+    e = golden["s20_ef8"]
+    roots = [0, e["roots64"][0]]
+    cases = [(2, "butterfly", r, True, d) for r in roots for d in ("top-down", "optimizing")]
+    world = 2
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_worker, args=(world, _free_port(), cases, out, 20), nprocs=world,
+                           join=True, start_method="spawn")
+        per_rank = [json.load(open(os.path.join(out, f"rank{r}.json"))) for r in range(world)]
+        for i, (_, _, root, _, direction) in enumerate(cases):
+            want = e["bfs"][str(root)]
+            for r in range(world):
+                lv = np.load(os.path.join(out, f"lv_{r}_{i}.npy"))
+                assert util.sha16(lv) == want["levels_sha"], (root, direction, r)
+                assert per_rank[r][i]["sizes"] == want["sizes"]
+                assert per_rank[r][i]["te"] == want["traversed_edges"]
+
+
+def _alpha_worker(rank, world, port, alphas, out_dir):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2103_13577_b200 import dist as bd
+    from paper_2103_13577_b200 import graphs
+
+    comm = bd.Comm()
+    g = graphs.kronecker(16, 8, 1, device=0)
+    dg = g.device
+    b = dg.partition_1d(world)
+    eng = bd.RankEngine(dg, b, 2, "butterfly", parents=True, comm=comm)
+    res = []
+    for a in alphas:
+        dg.set_direction("optimizing", alpha=a, beta=24.0)
+        d, st = eng.run(0)
+        np.save(os.path.join(out_dir, f"lv_{rank}_{len(res)}.npy"), d.d)
+        res.append({"bu": eng.node.last_bottom_up_levels, "chk": eng.node.last_switch_checksum,
+                    "sizes": st.per_level_frontier_size})
+        comm.barrier()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
+        json.dump(res, fh)
+    dist.destroy_process_group()
+
+
+def test_rank_direction_switch_agrees_across_ranks():
+    """Direction-optimizing rank mode decides top-down vs bottom-up on each
+    rank from global quantities; partition_1d bounds are not 32-aligned, so
+    the neighbours' bits of the boundary words must be in every rank's sum.
+    A sweep of alpha through the switching range puts some runs right at the
+    threshold: every rank must take the same number of bottom-up levels, and
+    the levels must equal the oracle BFS."""
+    world = 3
+    alphas = [float(a) for a in np.geomspace(0.5, 200.0, 24)]
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_alpha_worker, args=(world, _free_port(), alphas, out), nprocs=world,
+                           join=True, start_method="spawn")
+        per_rank = [json.load(open(os.path.join(out, f"rank{r}.json"))) for r in range(world)]
+        off, adj = util.rmat_graph(16)
+        ref = ob.bfs_top_down(off, adj, 0)
+        b = og.partition_1d(off, world)
+        assert any(x % 32 for x in b[1:-1])
+        for i, a in enumerate(alphas):
+            bus = {per_rank[r][i]["bu"] for r in range(world)}
+            assert len(bus) == 1, (a, bus)
+            # the rule's input, level by level, is the same global number
+            chks = {per_rank[r][i]["chk"] for r in range(world)}
+            assert len(chks) == 1 and chks.pop() > 0, (a, chks)
+            for r in range(world):
+                assert np.array_equal(np.load(os.path.join(out, f"lv_{r}_{i}.npy")), ref), (a, r)
+        assert len({per_rank[0][i]["bu"] for i in range(len(alphas))}) > 1  # the sweep switches

@@ -109,7 +109,9 @@ def test_partition_errors_and_spec_example():
         graphs.partition_1d(g, 5)
 
 
-def test_reference_graph_types_accepted(reference_graphs):
-    R = reference_graphs
-    rg = R.build_csr(R.symmetrize(R.generate_rmat(10, 8, 1)))
-    assert np.array_equal(graphs.partition_1d(rg, 4).boundaries, R.partition_1d(rg, 4).boundaries)
+def test_reference_graph_types_accepted(reference_objects):
+    rg, rp, _, _ = reference_objects("s10_ef8_seed1")
+    assert np.array_equal(graphs.partition_1d(rg, 4).boundaries, rp.boundaries)
+    dg = graphs.device_graph(rg)
+    off, adj = dg.csr()
+    assert np.array_equal(off, rg.offsets) and np.array_equal(adj, rg.adjacency)
