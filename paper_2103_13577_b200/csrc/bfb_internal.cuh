@@ -135,8 +135,14 @@ constexpr uint64_t kPcgMultLo = 0x4385DF649FCCF645ULL;
 // ------------------------------------------------------------ graph -------
 struct DevGraph {
   int64_t n = 0, m = 0, max_degree = 0;
-  DevBuf<int64_t> offsets;   // n+1
-  DevBuf<uint32_t> adj;      // m
+  DevBuf<int64_t> offsets;   // n+1 (always the whole graph)
+  DevBuf<uint32_t> adj;      // adjacency of rows [row_lo, row_hi) (all m entries when full)
+  // A partitioned build (one rank's share, bfb_graph_from_rmat_part) keeps
+  // only its own rows' adjacency: entries [adj_lo, adj_lo + adj.n) of the
+  // global adjacency; kernels index it with adj_index() and global offsets.
+  int64_t row_lo = 0, row_hi = 0, adj_lo = 0;
+  bool full() const { return row_lo == 0 && row_hi == n; }
+  const uint32_t* adj_index() const { return adj.p - adj_lo; }
   DevBuf<uint32_t> nonisol;  // bitmap of degree > 0 (bottom-up candidates), built at engine setup
   DevBuf<uint16_t> deg16;    // min(degree, 65535) per vertex (commit degree sums), engine setup
   DevBuf<uint2> first_nbr;    // two lowest-id neighbours per vertex (bottom-up first probes), engine setup
@@ -249,6 +255,15 @@ struct bfb_ctx {
   // result read-out: packed levels on device, staging in host memory
   bfb::DevBuf<uint32_t> packed;
   bfb::HostStage stage;
+  // the engine's degree-ordered relabel of the graph (relabel.cu), kept
+  // across engine setups with the same partition: eg = relabelled CSR,
+  // perm = old -> new id, inv = new -> old id; results are mapped back to
+  // the caller's ids into out_level / out_parent
+  bool relabeled = false;
+  std::vector<int64_t> relabel_bounds;
+  bfb::DevGraph eg;
+  bfb::DevBuf<uint32_t> perm, inv;
+  bfb::DevBuf<uint32_t> out_level, out_parent;
 };
 
 namespace bfb {
@@ -263,6 +278,10 @@ int rmat_to_host(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc, cons
 int load_csr(bfb_ctx* ctx, int64_t n, int64_t m, const int64_t* offsets, const uint32_t* adj);
 int build_from_device_edges(bfb_ctx* ctx, int64_t n, DevBuf<uint2>& edges, int64_t m,
                             bool symmetrize);
+// one rank's share of the RMAT graph: the whole offsets (every vertex's
+// degree) and only the adjacency of its partition_1d(parts) rows
+int build_from_rmat_part(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc,
+                         const uint64_t thr[3], int parts, int rank, int64_t* bounds_out);
 // ingest.cu
 int parse_text(bfb_ctx* ctx, const char* data, int64_t len, int fmt, int nl, int64_t line0,
                int64_t rows, int64_t cols, bfb_parse_result* res);
@@ -279,6 +298,15 @@ int read_levels(bfb_ctx* ctx, const uint32_t* level, int64_t n, int64_t num_leve
                 uint32_t* out, cudaStream_t s);
 int read_parents(bfb_ctx* ctx, const uint32_t* parent, int64_t n, int64_t* out, cudaStream_t s);
 int select_nonisolated(bfb_ctx* ctx, const int64_t* ranks, int64_t k, int64_t* out);
+
+// relabel.cu: the engine's degree-ordered relabel (within the parts of `bounds`)
+bool relabel_wanted(const bfb_ctx* ctx);
+int relabel_build(bfb_ctx* ctx, const std::vector<int64_t>& bounds);
+void relabel_release(bfb_ctx* ctx);
+// segsort.cu: per-row ascending sort of rows[rowstart[v]..rowstart[v+1]) into
+// out (hand-written warp bitonic / block radix); clobbers rows
+int sort_rows(bfb_ctx* ctx, const int64_t* rowstart, int64_t n, int64_t total, uint32_t* rows,
+              uint32_t* out);
 
 // scan.cu: exclusive scan of n values produced by a loader -> int64 out[0..n]
 // (out[n] = total).  Work buffers are sized by the caller via scan_tmp_words.

@@ -80,9 +80,16 @@ struct PartView {
   const uint16_t* deg16;    // min(degree, 65535)
   const uint2* first_nbr;    // two lowest-id neighbours (kNone if absent)
   const uint32_t* adj;       // CSR adjacency (the commit's parent pass)
+  const uint32_t* inv;       // relabelled engine graph: engine id -> caller's id (parents are
+                             // stored in the caller's ids), nullptr = identity
   bool rest_degrees;         // k_commit_rest also sums the degrees of its new vertices
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
+
+// The graph the engine traverses: the degree-ordered relabel when built
+// (relabel.cu), else the resident graph itself.
+DevGraph& EG(bfb_ctx* ctx) { return ctx->relabeled ? ctx->eg : ctx->g; }
+const uint32_t* perm_of(bfb_ctx* ctx) { return ctx->relabeled ? ctx->perm.p : nullptr; }
 
 PartView view_of(bfb_ctx* ctx, Part& p) {
   PartView v;
@@ -113,11 +120,13 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.tdeg = v.tcnt + nt;
   v.rebuild = false;
   v.ctr = p.ctr.p;
-  v.off = ctx->g.offsets.p;
-  v.nonisol = ctx->g.nonisol.p;
-  v.deg16 = ctx->g.deg16.p;
-  v.first_nbr = ctx->g.first_nbr.p;
-  v.adj = ctx->g.adj.p;
+  DevGraph& G = EG(ctx);
+  v.off = G.offsets.p;
+  v.nonisol = G.nonisol.p;
+  v.deg16 = G.deg16.p;
+  v.first_nbr = G.first_nbr.p;
+  v.adj = G.adj_index();
+  v.inv = ctx->relabeled ? ctx->inv.p : nullptr;
   v.rest_degrees = false;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
@@ -132,9 +141,18 @@ PartView commit_view_of(bfb_ctx* ctx, Part& p, uint32_t next_level) {
   return v;
 }
 
+// A vertex id as the caller sees it (parents are stored in the caller's ids,
+// so the output needs no id translation of its values).
+__device__ __forceinline__ uint32_t caller_id(const PartView& v, uint32_t x) {
+  return v.inv ? __ldg(v.inv + x) : x;
+}
+
 // ----------------------------------------------------------------- init ---
-__global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root, int owner,
-                       RunCounters* run) {
+// root: the caller's id; perm (relabelled engine graph) maps it to the
+// engine's id on device, so no host round trip precedes the launch.
+__global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root_in,
+                       const uint32_t* __restrict__ perm, int owner, RunCounters* run) {
+  const int64_t root = perm ? (int64_t)perm[root_in] : root_in;
   const int64_t w = root >> 5;
   const uint32_t b = 1u << (root & 31);
   if (threadIdx.x == 0) {
@@ -142,7 +160,7 @@ __global__ void k_seed(PartView v, const int64_t* __restrict__ off, int64_t root
     v.start[w] = b;
     if (v.front) v.front[w] = b;
     v.level[root] = 0;
-    if (v.parent) v.parent[root] = (uint32_t)root;
+    if (v.parent) v.parent[root] = (uint32_t)root_in;  // parents hold the caller's ids
     PartCounters c{};
     if (owner) {
       int64_t d = off[root + 1] - off[root];
@@ -283,7 +301,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
       atomicOr(&visited[u[it] >> 5], bit);
       if (kParents) {
         const uint32_t ro = (rows[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
-        v.parent[u[it]] = __ldg(v.q_v + vs + ro);
+        v.parent[u[it]] = caller_id(v, __ldg(v.q_v + vs + ro));
       }
     }
   }
@@ -303,7 +321,7 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
                                                int64_t e0, int span, uint32_t row, uint64_t pol) {
   const int lane = threadIdx.x & 31;
   const int64_t base = __ldg(v.q_base + row) + e0;
-  const uint32_t src = kParents ? __ldg(v.q_v + row) : 0u;
+  const uint32_t src = kParents ? caller_id(v, __ldg(v.q_v + row)) : 0u;
   uint32_t* __restrict__ visited = v.visited;
   for (int k = 0; k < span; k += 32 * kRunItems) {
     uint32_t u[kRunItems], wv[kRunItems];
@@ -676,7 +694,7 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
               }
             }
           }
-          v.parent[u[b]] = p;
+          v.parent[u[b]] = p == kNone ? kNone : caller_id(v, p);
         }
       }
       __syncwarp();
@@ -1138,7 +1156,7 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
       }
       const uint32_t nbits = __ballot_sync(0xffffffffu, found);
       if (lane == 0 && nbits) v.visited[w] = vis | nbits;  // this node is the word's only writer
-      if (kParents && found) v.parent[u] = par;
+      if (kParents && found) v.parent[u] = caller_id(v, par);
     }
   }
   ex = (unsigned long long)warp_sum_i64((int64_t)ex);
@@ -1264,6 +1282,47 @@ __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __rest
 }
 
 // ------------------------------------------------------------ outputs ----
+// Results in the caller's ids (relabelled engine graph): out[v] = engine
+// result at perm[v], after d_local was materialised in engine ids.  The
+// relabel keeps each degree class in the caller's order, so consecutive v
+// gather from a few ascending streams (isolated vertices: one stream of
+// UNREACHED); each thread keeps kOutBatch vertices' loads in flight (the
+// perm -> gather chain is latency-bound otherwise: 6.6 ms vs 1.x ms at s29).
+// Parents are stored in the caller's ids already; an unreached vertex gets
+// none (this also masks a single node's stale entries).  out_level ==
+// nullptr: parents only.
+constexpr int kOutBatch = 8;
+__global__ void __launch_bounds__(256) k_output(const uint32_t* __restrict__ perm,
+                                                const uint32_t* __restrict__ level,
+                                                const uint32_t* __restrict__ parent,
+                                                uint32_t* __restrict__ out_level,
+                                                uint32_t* __restrict__ out_parent, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < n;
+       v0 += stride * kOutBatch) {
+    uint32_t p[kOutBatch], l[kOutBatch], q[kOutBatch];
+#pragma unroll
+    for (int k = 0; k < kOutBatch; ++k) {
+      const int64_t v = v0 + k * stride;
+      p[k] = v < n ? __ldg(perm + v) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kOutBatch; ++k) l[k] = v0 + k * stride < n ? __ldg(level + p[k]) : kNone;
+    if (out_parent) {
+#pragma unroll
+      for (int k = 0; k < kOutBatch; ++k) q[k] = l[k] != kNone ? __ldg(parent + p[k]) : kNone;
+    }
+#pragma unroll
+    for (int k = 0; k < kOutBatch; ++k) {
+      const int64_t v = v0 + k * stride;
+      if (v < n) {
+        if (out_level) out_level[v] = l[k];
+        if (out_parent) out_parent[v] = q[k];
+      }
+    }
+  }
+}
+
 __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n, uint32_t* out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1277,8 +1336,8 @@ __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n
 // Per-vertex tables built once per engine setup (lane = vertex): the bitmap
 // of degree > 0 and min(degree, 65535) as 16 bits.
 __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                int64_t n, uint32_t* nonisol, uint16_t* deg16, uint2* first_nbr,
-                                int64_t nwords_pad) {
+                                int64_t n, int64_t row_lo, int64_t row_hi, uint32_t* nonisol,
+                                uint16_t* deg16, uint2* first_nbr, int64_t nwords_pad) {
   const int lane = threadIdx.x & 31;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords_pad;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -1288,9 +1347,14 @@ __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t*
     const unsigned b = __ballot_sync(0xffffffffu, d > 0);
     if (lane == 0) nonisol[w] = b;
     deg16[u] = (uint16_t)min(d, (int64_t)0xFFFF);
-    first_nbr[u] = make_uint2(d > 0 ? __ldg(adj + o) : kNone, d > 1 ? __ldg(adj + o + 1) : kNone);
+    // (a rank's partitioned graph holds only its own rows' adjacency; the
+    // tables of the other rows are never read)
+    const bool mine = u >= row_lo && u < row_hi;
+    first_nbr[u] = make_uint2(mine && d > 0 ? __ldg(adj + o) : kNone,
+                              mine && d > 1 ? __ldg(adj + o + 1) : kNone);
   }
 }
+
 
 // Single-node runs skip the 2 GB parent reset: every reached vertex but the
 // root gets its parent from its own claim, so only unreached vertices hold
@@ -1383,6 +1447,7 @@ unsigned grid_cap(int64_t work, int block, int num_sms, int per_sm = 8) {
   return (unsigned)g;
 }
 
+
 // d_local from the level bitmaps at termination (last_level = the deepest
 // level committed); returns kernels launched.
 int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStream_t s) {
@@ -1392,6 +1457,18 @@ int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStr
                                      ctx->num_sms),
                        256, 0, s>>>(p.lvbits.p, pad, nl, p.visited.p, p.level.p, ctx->g.n);
   return 1;
+}
+
+// Node 0's results in the caller's ids (relabelled engine graph).
+int launch_output(bfb_ctx* ctx, Part& p, int64_t last_level, const uint32_t* parent, bool levels,
+                  cudaStream_t s) {
+  int k = 0;
+  if (levels) k += launch_materialise_levels(ctx, p, last_level, s);
+  const int64_t n = ctx->g.n;
+  k_output<<<grid_cap((n + kOutBatch - 1) / kOutBatch, 256, ctx->num_sms, 8), 256, 0, s>>>(
+      ctx->perm.p, p.level.p, parent, levels ? ctx->out_level.p : nullptr,
+      parent ? ctx->out_parent.p : nullptr, n);
+  return k + 1;
 }
 
 // Multi-process merge: OR the round's source snapshots (peer memory mapped
@@ -1519,6 +1596,11 @@ struct EngineTables {
 
 bool rank_mode(const bfb_ctx* ctx) { return ctx->tables && ctx->tables->rank >= 0; }
 
+// d_local of node 0 in the caller's ids
+static const uint32_t* out_levels(bfb_ctx* ctx) {
+  return ctx->relabeled ? ctx->out_level.p : ctx->parts[0].level.p;
+}
+
 void engine_release(bfb_ctx* ctx) {
   ctx->parts.clear();
   ctx->run.release();
@@ -1533,9 +1615,24 @@ void engine_release(bfb_ctx* ctx) {
   ctx->tables = nullptr;
 }
 
+// rb: the partition the engine graph is relabelled within (the engine's own
+// partition, or the global one for a rank's single-node engine)
+static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout,
+                           int strategy, int want_parents, const std::vector<int64_t>& rb);
+
 int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int strategy,
                  int want_parents) {
+  if (parts < 1) return fail(BFB_ERR_PARTITION, "num_parts must be >= 1");
+  if (ctx->g.valid && !ctx->g.full())
+    return fail(BFB_ERR_STATE, "this context holds one rank's rows only (use bfb_rank_setup)");
+  return engine_setup_rb(ctx, parts, bounds, fanout, strategy, want_parents,
+                         std::vector<int64_t>(bounds, bounds + parts + 1));
+}
+
+static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout,
+                           int strategy, int want_parents, const std::vector<int64_t>& rb) {
   if (!ctx->g.valid) return fail(BFB_ERR_STATE, "no graph loaded");
+
   const int64_t n = ctx->g.n;
   if (parts < 1) return fail(BFB_ERR_PARTITION, "num_parts must be >= 1");
   if (bounds[0] != 0 || bounds[parts] != n)
@@ -1564,12 +1661,23 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
       BFB_CUDA(cudaMemcpy(&off_h[g], ctx->g.offsets.p + bounds[g], sizeof(int64_t),
                           cudaMemcpyDeviceToHost));
   }
-  BFB_TRY(ctx->g.nonisol.alloc(nwords_pad));
-  BFB_TRY(ctx->g.deg16.alloc((size_t)nwords_pad * 32));
-  BFB_TRY(ctx->g.first_nbr.alloc((size_t)nwords_pad * 32));
+  // the engine's graph: degree-ordered within the parts of rb (relabel.cu)
+  if (relabel_wanted(ctx)) {
+    BFB_TRY(relabel_build(ctx, rb));
+  } else {
+    relabel_release(ctx);
+  }
+  DevGraph& G = EG(ctx);
+  BFB_TRY(G.nonisol.alloc(nwords_pad));
+  BFB_TRY(G.deg16.alloc((size_t)nwords_pad * 32));
+  BFB_TRY(G.first_nbr.alloc((size_t)nwords_pad * 32));
   k_vertex_tables<<<grid_cap(nwords_pad * 32, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
-      ctx->g.offsets.p, ctx->g.adj.p, n, ctx->g.nonisol.p, ctx->g.deg16.p, ctx->g.first_nbr.p,
+      G.offsets.p, G.adj_index(), n, G.row_lo, G.row_hi, G.nonisol.p, G.deg16.p, G.first_nbr.p,
       nwords_pad);
+  if (ctx->relabeled) {
+    BFB_TRY(ctx->out_level.alloc(n + 1));
+    if (want_parents) BFB_TRY(ctx->out_parent.alloc(n + 1));
+  }
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->parts.resize(parts);
   std::vector<uint32_t*> pubs(parts), viss(parts), pars(parts);
@@ -1679,7 +1787,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   const int P = ctx->num_parts;
   const int sms = ctx->num_sms;
   const int64_t nwords = (n + 31) / 32;
-  const int64_t* off = ctx->g.offsets.p;
+  const int64_t* off = EG(ctx).offsets.p;
   int64_t launches = 0;
   double t_expand = 0, t_exchange = 0, t_commit = 0, t_expand_max = 0;
   int64_t expand_launches = 0;
@@ -1701,7 +1809,8 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     if (ctx->want_parents && P > 1)
       BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
     if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
-    k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), off, root, g == owner ? 1 : 0, ctx->run.p);
+    k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), off, root, perm_of(ctx), g == owner ? 1 : 0,
+                             ctx->run.p);
     ++launches;
   }
   // Direction-optimizing state (Beamer's heuristic): switch to bottom-up when
@@ -1740,13 +1849,13 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
         const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
         unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
         if (ctx->want_parents)
-          k_bottom_up<true><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+          k_bottom_up<true><<<bg, 256, 0, s>>>(v, EG(ctx).adj_index(), ex);
         else
-          k_bottom_up<false><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+          k_bottom_up<false><<<bg, 256, 0, s>>>(v, EG(ctx).adj_index(), ex);
       } else if (expand_parents) {
-        launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, s);
+        launch_expand<true>(ctx->expand_grid, v, EG(ctx).adj_index(), s);
       } else {
-        launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, s);
+        launch_expand<false>(ctx->expand_grid, v, EG(ctx).adj_index(), s);
       }
       ++launches;
       ++expand_launches;
@@ -1875,8 +1984,10 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     ++level;
     if (level > n) return fail(BFB_ERR_CAPACITY, "level count exceeded |V| (internal error)");
   }
-  for (int g = 0; g < P; ++g) launches += launch_materialise_levels(ctx, ctx->parts[g], level + 1, s);
-  BFB_CUDA(cudaEventRecord(D->ev[1], s));
+  // d_local at termination (the relabelled engine writes node 0's straight
+  // into the caller's ids below)
+  if (!ctx->relabeled)
+    for (int g = 0; g < P; ++g) launches += launch_materialise_levels(ctx, ctx->parts[g], level + 1, s);
   // Parents of the output view: any node's phase-1 claim is a valid parent.
   const uint32_t* parents_dev = nullptr;
   if (ctx->want_parents) {
@@ -1886,21 +1997,29 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       k_parents_min<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(D->parents.p, P, n,
                                                              D->parents_final.p);
       parents_dev = D->parents_final.p;
+      ++launches;
     }
   }
+  // results in the caller's ids (relabelled engine graph), inside the timed
+  // region: levels and parents final on device
+  if (ctx->relabeled) {
+    launches += launch_output(ctx, ctx->parts[0], level + 1, parents_dev, true, s);
+    if (parents_dev) parents_dev = ctx->out_parent.p;
+  }
+  BFB_CUDA(cudaEventRecord(D->ev[1], s));
   // Stats
   RunCounters rc;
   BFB_CUDA(cudaMemcpyAsync(&rc, ctx->run.p, sizeof(rc), cudaMemcpyDeviceToHost, s));
   std::vector<int64_t> hw(P);
   BFB_CUDA(cudaMemcpyAsync(hw.data(), ctx->high_water.p, P * sizeof(int64_t),
                            cudaMemcpyDeviceToHost, s));
-  if (levels_out) BFB_TRY(read_levels(ctx, ctx->parts[0].level.p, n, nsizes, levels_out, s));
+  if (levels_out) BFB_TRY(read_levels(ctx, out_levels(ctx), n, nsizes, levels_out, s));
   BFB_CUDA(cudaStreamSynchronize(s));
   float elapsed = 0;
   BFB_CUDA(cudaEventElapsedTime(&elapsed, D->ev[0], D->ev[1]));
   if (parents_out) {
     if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
-    if (P == 1)
+    if (P == 1 && !ctx->relabeled)  // (the un-permute masked them already)
       k_mask_parents<<<grid_cap(n, 256, sms, 8), 256, 0, s>>>(ctx->parts[0].level.p,
                                                               ctx->parts[0].parent.p, n);
     BFB_TRY(read_parents(ctx, parents_dev, n, parents_out, s));
@@ -1942,7 +2061,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
 
 int engine_copy_levels(bfb_ctx* ctx, uint32_t* out) {
   if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
-  BFB_TRY(read_levels(ctx, ctx->parts[0].level.p, ctx->g.n, ctx->last_levels, out, ctx->stream));
+  BFB_TRY(read_levels(ctx, out_levels(ctx), ctx->g.n, ctx->last_levels, out, ctx->stream));
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   return BFB_OK;
 }
@@ -1950,6 +2069,10 @@ int engine_copy_levels(bfb_ctx* ctx, uint32_t* out) {
 // Device array of the last run's output parents (kNone where unreached).
 static int output_parents(bfb_ctx* ctx, const uint32_t** out) {
   EngineTables* D = ctx->tables;
+  if (ctx->relabeled) {  // mapped back (and masked) by the run's un-permute
+    *out = ctx->out_parent.p;
+    return BFB_OK;
+  }
   if (ctx->num_parts > 1) {
     *out = D->parents_final.p;
     return BFB_OK;
@@ -1974,13 +2097,15 @@ int engine_copy_parents(bfb_ctx* ctx, int64_t* out) {
 
 int engine_validate(bfb_ctx* ctx, int64_t root, int64_t* errs) {
   if (!ctx->have_run) return fail(BFB_ERR_STATE, "no BFS has run");
+  if (!ctx->g.full()) return fail(BFB_ERR_STATE, "the certificate needs the whole graph");
   const uint32_t* par = nullptr;
   if (ctx->want_parents) BFB_TRY(output_parents(ctx, &par));
   DevBuf<unsigned> err;
   BFB_TRY(err.alloc(1));
   BFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(unsigned), ctx->stream));
+  // the caller's graph and ids: independent of the engine's relabel
   k_validate<<<grid_cap(ctx->g.n * 32, 256, ctx->num_sms, 16), 256, 0, ctx->stream>>>(
-      ctx->g.offsets.p, ctx->g.adj.p, ctx->g.n, ctx->parts[0].level.p, par, root, err.p);
+      ctx->g.offsets.p, ctx->g.adj.p, ctx->g.n, out_levels(ctx), par, root, err.p);
   unsigned h = 0;
   BFB_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1999,6 +2124,7 @@ __global__ void k_parents_from_i64(const int64_t* __restrict__ in, uint32_t* __r
 
 int validate_host(bfb_ctx* ctx, int64_t root, const uint32_t* levels, const int64_t* parents,
                   int64_t* errs) {
+  if (!ctx->g.full()) return fail(BFB_ERR_STATE, "the certificate needs the whole graph");
   const int64_t n = ctx->g.n;
   cudaStream_t s = ctx->stream;
   DevBuf<uint32_t> lv, par;
@@ -2033,15 +2159,18 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
                int want_parents, int rank) {
   if (rank < 0 || rank >= parts) return fail(BFB_ERR_INVALID, "rank out of range");
   if (parts > kMaxSrc) return fail(BFB_ERR_INVALID, "at most 64 nodes in multi-process mode");
-  // Validate and allocate as a single-node engine over the local part, then
-  // re-label it with the global partition.
-  BFB_TRY(engine_setup(ctx, 1, std::vector<int64_t>{0, ctx->g.n}.data(), 1, strategy,
-                       want_parents));
   const int64_t n = ctx->g.n;
   if (bounds[0] != 0 || bounds[parts] != n)
     return fail(BFB_ERR_PARTITION, "partition does not match graph");
   for (int g = 0; g < parts; ++g)
     if (bounds[g + 1] < bounds[g]) return fail(BFB_ERR_PARTITION, "partition does not match graph");
+  if (!ctx->g.full() && (ctx->g.row_lo != bounds[rank] || ctx->g.row_hi != bounds[rank + 1]))
+    return fail(BFB_ERR_PARTITION, "this context holds the rows of another part");
+  // Validate and allocate as a single-node engine over the local part, then
+  // re-label it with the global partition.  The engine graph is relabelled
+  // within the GLOBAL partition, so every rank holds the same relabel.
+  BFB_TRY(engine_setup_rb(ctx, 1, std::vector<int64_t>{0, ctx->g.n}.data(), 1, strategy,
+                          want_parents, std::vector<int64_t>(bounds, bounds + parts + 1)));
   if (fanout < 1 || fanout > parts) return fail(BFB_ERR_FANOUT, "fanout exceeds num_nodes");
   BFB_TRY(make_schedule(parts, fanout, strategy, ctx->schedule));
   ctx->num_parts = parts;
@@ -2144,7 +2273,8 @@ int rank_begin(bfb_ctx* ctx, int64_t root) {
   if (ctx->want_parents) BFB_CUDA(cudaMemsetAsync(p.parent.p, 0xFF, n * sizeof(uint32_t), s));
   if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
   const int owner = root >= p.lo && root < p.hi;
-  k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), ctx->g.offsets.p, root, owner, ctx->run.p);
+  k_seed<<<1, 256, 0, s>>>(view_of(ctx, p), EG(ctx).offsets.p, root, perm_of(ctx), owner,
+                           ctx->run.p);
   BFB_CUDA(cudaGetLastError());
   D->level = 0;
   D->levels = 1;
@@ -2159,9 +2289,9 @@ int rank_begin(bfb_ctx* ctx, int64_t root) {
 int rank_expand(bfb_ctx* ctx) {
   PartView v = view_of(ctx, ctx->parts[0]);
   if (ctx->want_parents)
-    launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, ctx->stream);
+    launch_expand<true>(ctx->expand_grid, v, EG(ctx).adj_index(), ctx->stream);
   else
-    launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, ctx->stream);
+    launch_expand<false>(ctx->expand_grid, v, EG(ctx).adj_index(), ctx->stream);
   ++ctx->tables->launches;
   BFB_CUDA(cudaGetLastError());
   return BFB_OK;
@@ -2220,7 +2350,7 @@ int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
   k_commit_prep<<<1, 32, 0, s>>>(D->ctrs.p, 1);
   ++D->launches;
   if (p.whi > p.wlo) {
-    D->launches += launch_commit(v, ctx->g.offsets.p, next_level, ctx->run.p, ctx->num_sms, s);
+    D->launches += launch_commit(v, EG(ctx).offsets.p, next_level, ctx->run.p, ctx->num_sms, s);
   }
   if (nwords - (p.whi - p.wlo) > 0) {
     k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, ctx->num_sms), 256, 0, s>>>(v, next_level);
@@ -2244,7 +2374,10 @@ int rank_commit(bfb_ctx* ctx, int64_t* frontier_out, int64_t* owned_out) {
 int rank_finish(bfb_ctx* ctx, bfb_run_stats* st) {
   EngineTables* D = ctx->tables;
   cudaStream_t s = ctx->stream;
-  D->launches += launch_materialise_levels(ctx, ctx->parts[0], D->level + 1, s);
+  if (ctx->relabeled)
+    D->launches += launch_output(ctx, ctx->parts[0], D->level + 1, nullptr, true, s);
+  else
+    D->launches += launch_materialise_levels(ctx, ctx->parts[0], D->level + 1, s);
   BFB_CUDA(cudaEventRecord(D->ev[1], s));
   RunCounters rc;
   BFB_CUDA(cudaMemcpyAsync(&rc, ctx->run.p, sizeof(rc), cudaMemcpyDeviceToHost, s));
@@ -2285,15 +2418,25 @@ int rank_parents(bfb_ctx* ctx, int64_t* out) {
   const int64_t n = ctx->g.n;
   k_parents_min<<<grid_cap(n, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
       D->parents.p, P, n, D->parents_final.p);
-  BFB_TRY(read_parents(ctx, D->parents_final.p, n, out, ctx->stream));
+  const uint32_t* src = D->parents_final.p;
+  if (ctx->relabeled) {
+    launch_output(ctx, ctx->parts[0], D->level + 1, D->parents_final.p, false, ctx->stream);
+    src = ctx->out_parent.p;
+  }
+  BFB_TRY(read_parents(ctx, src, n, out, ctx->stream));
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
   return BFB_OK;
 }
 
 int rank_parents_raw(bfb_ctx* ctx, uint32_t* out) {
   if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
-  BFB_CUDA(cudaMemcpy(out, ctx->parts[0].parent.p, ctx->g.n * sizeof(uint32_t),
-                      cudaMemcpyDeviceToHost));
+  const uint32_t* src = ctx->parts[0].parent.p;
+  if (ctx->relabeled) {  // this node's claims at the caller's ids
+    launch_output(ctx, ctx->parts[0], ctx->tables->level + 1, src, false, ctx->stream);
+    BFB_CUDA(cudaStreamSynchronize(ctx->stream));
+    src = ctx->out_parent.p;
+  }
+  BFB_CUDA(cudaMemcpy(out, src, ctx->g.n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return BFB_OK;
 }
 
@@ -2475,7 +2618,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   cudaStream_t s = ctx->stream;
   Part& p = ctx->parts[0];
   const int64_t n = ctx->g.n, nwords = (n + 31) / 32;
-  const int64_t* off = ctx->g.offsets.p;
+  const int64_t* off = EG(ctx).offsets.p;
   const int sms = ctx->num_sms;
   const int64_t bytes_per_transfer = nwords * (int64_t)sizeof(uint32_t);
   const uint64_t timeout_ns = 60ull * 1000 * 1000 * 1000;
@@ -2497,7 +2640,8 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   int64_t switch_chk = 0;
   if (ctx->direction == 1) {
     int64_t ob[2];
-    BFB_CUDA(cudaMemcpy(ob, off + root, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    // the root's degree (the caller's graph: the relabel keeps degrees)
+    BFB_CUDA(cudaMemcpy(ob, ctx->g.offsets.p + root, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
     seen_edges = ob[1] - ob[0];
   }
   if (sizes_out && max_levels > 0) sizes_out[0] = 1;
@@ -2516,14 +2660,14 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
       unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
       if (ctx->want_parents)
-        k_bottom_up<true><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+        k_bottom_up<true><<<bg, 256, 0, s>>>(v, EG(ctx).adj_index(), ex);
       else
-        k_bottom_up<false><<<bg, 256, 0, s>>>(v, ctx->g.adj.p, ex);
+        k_bottom_up<false><<<bg, 256, 0, s>>>(v, EG(ctx).adj_index(), ex);
       ++bu_levels;
     } else if (ctx->want_parents && !parent_pass) {
-      launch_expand<true>(ctx->expand_grid, v, ctx->g.adj.p, s);
+      launch_expand<true>(ctx->expand_grid, v, EG(ctx).adj_index(), s);
     } else {
-      launch_expand<false>(ctx->expand_grid, v, ctx->g.adj.p, s);
+      launch_expand<false>(ctx->expand_grid, v, EG(ctx).adj_index(), s);
     }
     ++launches;
     ++expand_launches;

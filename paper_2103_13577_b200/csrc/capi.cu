@@ -189,6 +189,7 @@ void bfb_destroy(bfb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   engine_release(ctx);
+  relabel_release(ctx);
   ctx->g = DevGraph();
   for (auto& e : ctx->timer)
     if (e) cudaEventDestroy(e);

@@ -6,14 +6,12 @@
 //   count   : degree histogram of the (mirrored, self-loop-free) edges
 //   scan    : row starts (int64)
 //   scatter : each edge appended to its row (atomic row cursor)
-//   sort    : per-row sort (cub::DeviceSegmentedSort, chunked below 2^31 items)
+//   sort    : per-row sort (segsort.cu: warp bitonic, block radix for long rows)
 //   flag    : first-of-row or differs-from-predecessor, packed 32 per word
 //   scan    : popcount prefix -> deduplicated offsets; compact.
 // The RMAT source is regenerated for the count and scatter passes instead of
 // being stored (2 x 17 GB saved at scale 29); PCG64 jump-ahead makes any draw
 // index addressable.
-#include <cub/device/device_segmented_sort.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
 
 #include <algorithm>
 
@@ -42,10 +40,18 @@ struct RmatParams {
 struct BuildSink {
   uint2* edges;            // kModeEdges
   uint32_t* deg;           // kModeCount
-  const int64_t* rowstart; // kModeScatter
+  const int64_t* rowstart; // kModeScatter: rows [row_lo, row_hi) only, indexed from row_lo
   uint32_t* fill;
   uint32_t* rows;
+  int64_t row_lo, row_hi;
 };
+
+__device__ __forceinline__ void sink_row(const BuildSink& k, uint32_t s, uint32_t d) {
+  if ((int64_t)s < k.row_lo || (int64_t)s >= k.row_hi) return;
+  const int64_t r = (int64_t)s - k.row_lo;
+  const uint32_t p = atomicAdd(&k.fill[r], 1u);
+  k.rows[k.rowstart[r] + p] = d;
+}
 
 __device__ __forceinline__ void sink_edge(int mode, const BuildSink& k, int64_t e, uint32_t s,
                                           uint32_t d) {
@@ -56,10 +62,8 @@ __device__ __forceinline__ void sink_edge(int mode, const BuildSink& k, int64_t 
       atomicAdd(&k.deg[s], 1u);
       atomicAdd(&k.deg[d], 1u);
     } else {
-      uint32_t p = atomicAdd(&k.fill[s], 1u);
-      k.rows[k.rowstart[s] + p] = d;
-      uint32_t q = atomicAdd(&k.fill[d], 1u);
-      k.rows[k.rowstart[d] + q] = s;
+      sink_row(k, s, d);
+      sink_row(k, d, s);
     }
   }
 }
@@ -126,8 +130,7 @@ __global__ void k_edges(const uint2* __restrict__ edges, int64_t m, int64_t n, i
       if (MODE == kModeCount) {
         atomicAdd(&sink.deg[p.x], 1u);
       } else {
-        uint32_t q = atomicAdd(&sink.fill[p.x], 1u);
-        sink.rows[sink.rowstart[p.x] + q] = p.y;
+        sink_row(sink, p.x, p.y);
       }
     }
   }
@@ -225,15 +228,6 @@ __global__ void k_check_reverse(const int64_t* __restrict__ off, const uint32_t*
 }
 
 // Largest v in [lo, hi] with a[v] <= key (a non-decreasing).
-__global__ void k_search_le(const int64_t* __restrict__ a, int64_t lo, int64_t hi, int64_t key,
-                            int64_t* out) {
-  while (lo < hi) {
-    int64_t mid = lo + (hi - lo + 1) / 2;
-    if (a[mid] <= key) lo = mid; else hi = mid - 1;
-  }
-  out[0] = lo;
-  out[1] = a[lo];
-}
 
 __global__ void k_expand_edges(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                int64_t n, uint2* out) {
@@ -341,53 +335,10 @@ int launch_rmat(const RmatParams& P, const BuildSink& sink, cudaStream_t s) {
   return BFB_OK;
 }
 
-struct SubBase {
-  int64_t base;
-  __host__ __device__ __forceinline__ int operator()(const int64_t& x) const {
-    return (int)(x - base);
-  }
-};
 
-// Per-row ascending sort of rows[rowstart[v] .. rowstart[v+1]) into out,
-// chunked so each cub call stays below 2^31 items.
-int sort_rows(bfb_ctx* ctx, const int64_t* rowstart, int64_t n, int64_t total, const uint32_t* rows,
-              uint32_t* out) {
-  cudaStream_t s = ctx->stream;
-  const int64_t kLimit = (int64_t(1) << 30);
-  DevBuf<int64_t> probe;
-  BFB_TRY(probe.alloc(2));
-  DevBuf<char> tmp;
-  int64_t v0 = 0, p0 = 0;
-  while (v0 < n) {
-    int64_t v1, p1;
-    if (total - p0 <= kLimit && n - v0 <= kLimit) {
-      v1 = n;
-      p1 = total;
-    } else {
-      k_search_le<<<1, 1, 0, s>>>(rowstart, v0, std::min(n, v0 + kLimit), p0 + kLimit, probe.p);
-      int64_t h[2];
-      BFB_CUDA(cudaMemcpyAsync(h, probe.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-      BFB_CUDA(cudaStreamSynchronize(s));
-      v1 = h[0];
-      p1 = h[1];
-      if (v1 <= v0) return fail(BFB_ERR_INVALID, "row larger than the sort chunk limit");
-    }
-    int items = (int)(p1 - p0), segs = (int)(v1 - v0);
-    if (items > 0) {
-      cub::TransformInputIterator<int, SubBase, const int64_t*> beg(rowstart + v0, SubBase{p0});
-      cub::TransformInputIterator<int, SubBase, const int64_t*> end(rowstart + v0 + 1, SubBase{p0});
-      size_t bytes = 0;
-      BFB_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, rows + p0, out + p0, items, segs,
-                                                  beg, end, s));
-      if (bytes > tmp.n) BFB_TRY(tmp.alloc(bytes));
-      BFB_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, bytes, rows + p0, out + p0, items, segs,
-                                                  beg, end, s));
-    }
-    v0 = v1;
-    p0 = p1;
-  }
-  return BFB_OK;
-}
+}  // namespace
+
+namespace {
 
 // Shared tail of both build paths: rows are scattered, now sort, flag, dedup
 // (or validate), and install as the resident CSR.
@@ -410,6 +361,8 @@ int finish_build(bfb_ctx* ctx, int64_t n, DevBuf<uint32_t>& deg, ScatterFn scatt
   sink.rowstart = rowstart.p;
   sink.fill = deg.p;
   sink.rows = rows.p;
+  sink.row_lo = 0;
+  sink.row_hi = n;
   BFB_TRY(scatter(sink));
   deg.release();
   DevBuf<uint32_t> sorted;
@@ -476,16 +429,182 @@ int finish_build(bfb_ctx* ctx, int64_t n, DevBuf<uint32_t>& deg, ScatterFn scatt
   BFB_CUDA(cudaStreamSynchronize(s));
   BFB_CUDA(cudaGetLastError());
   engine_release(ctx);
+  relabel_release(ctx);
   ctx->g.offsets = std::move(offsets);
   ctx->g.adj = std::move(adj);
   ctx->g.n = n;
   ctx->g.m = m_final;
   ctx->g.max_degree = (int64_t)md;
+  ctx->g.row_lo = 0;
+  ctx->g.row_hi = n;
+  ctx->g.adj_lo = 0;
   ctx->g.valid = true;
   return BFB_OK;
 }
 
 }  // namespace
+
+namespace {
+
+__global__ void k_row_degrees(const int64_t* __restrict__ rel_off, int64_t cnt, uint32_t* deg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = (uint32_t)(rel_off[i + 1] - rel_off[i]);
+}
+
+// Rows [a, b) of the symmetrized, deduplicated RMAT graph, from the raw
+// degrees (count pass): scatter of the edges with an endpoint in [a, b),
+// per-row sort, duplicate flags.  Writes the rows' deduplicated degrees to
+// ddeg[a..b) and, when adj_out is given, their adjacency (compacted).
+int rmat_slice(bfb_ctx* ctx, const RmatParams& P, const uint32_t* deg, int64_t a, int64_t b,
+               uint32_t* ddeg, DevBuf<uint32_t>* adj_out) {
+  cudaStream_t s = ctx->stream;
+  const int sms = ctx->num_sms;
+  const int64_t ns = b - a;
+  if (ns <= 0) return BFB_OK;
+  DevBuf<int64_t> rowstart, tmp;
+  BFB_TRY(rowstart.alloc(ns + 1));
+  BFB_TRY(tmp.alloc(scan_tmp_words(ns) + 1));
+  BFB_TRY(scan_u32_to_i64(deg + a, ns, rowstart.p, tmp.p, s));
+  int64_t total = 0;
+  BFB_CUDA(cudaMemcpyAsync(&total, rowstart.p + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  BFB_CUDA(cudaStreamSynchronize(s));
+  DevBuf<uint32_t> rows, fill, sorted;
+  BFB_TRY(rows.alloc(total + 1));
+  BFB_TRY(fill.alloc(ns));
+  BFB_CUDA(cudaMemsetAsync(fill.p, 0, ns * sizeof(uint32_t), s));
+  BuildSink sink{};
+  sink.rowstart = rowstart.p;
+  sink.fill = fill.p;
+  sink.rows = rows.p;
+  sink.row_lo = a;
+  sink.row_hi = b;
+  BFB_TRY(launch_rmat<kModeScatter>(P, sink, s));
+  fill.release();
+  BFB_TRY(sorted.alloc(total + 1));
+  BFB_TRY(sort_rows(ctx, rowstart.p, ns, total, rows.p, sorted.p));
+  const int64_t nwords = (total + 31) / 32;
+  DevBuf<uint32_t> rs_bits, keep;
+  DevBuf<unsigned> err;
+  BFB_TRY(err.alloc(1));
+  BFB_TRY(rs_bits.alloc(nwords + 1));
+  BFB_TRY(keep.alloc(nwords + 1));
+  BFB_CUDA(cudaMemsetAsync(rs_bits.p, 0, (nwords + 1) * sizeof(uint32_t), s));
+  BFB_CUDA(cudaMemsetAsync(keep.p, 0, (nwords + 1) * sizeof(uint32_t), s));
+  k_mark_rowstarts<<<grid_for(ns, 256, sms), 256, 0, s>>>(rowstart.p, ns, rs_bits.p);
+  k_flag_unique<<<grid_for(nwords * 32, 256, sms), 256, 0, s>>>(sorted.p, total, rs_bits.p, keep.p,
+                                                               err.p);
+  rs_bits.release();
+  DevBuf<int64_t> word_pre, tmp2, rel_off;
+  DevBuf<unsigned long long> unused;
+  BFB_TRY(word_pre.alloc(nwords + 1));
+  BFB_TRY(tmp2.alloc(scan_tmp_words(nwords) + 1));
+  BFB_TRY(scan_popc_to_i64(keep.p, nwords, word_pre.p, tmp2.p, s));
+  BFB_TRY(rel_off.alloc(ns + 1));
+  BFB_TRY(unused.alloc(1));
+  k_new_offsets<<<grid_for(ns + 1, 256, sms), 256, 0, s>>>(rowstart.p, ns, keep.p, word_pre.p,
+                                                            rel_off.p, unused.p);
+  k_row_degrees<<<grid_for(ns, 256, sms), 256, 0, s>>>(rel_off.p, ns, ddeg + a);
+  if (adj_out) {
+    int64_t ms = 0;
+    BFB_CUDA(cudaMemcpyAsync(&ms, rel_off.p + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
+    BFB_TRY(adj_out->alloc(ms + 1));
+    k_compact<<<grid_for(total, 256, sms), 256, 0, s>>>(sorted.p, total, keep.p, word_pre.p,
+                                                        adj_out->p);
+  }
+  BFB_CUDA(cudaStreamSynchronize(s));
+  BFB_CUDA(cudaGetLastError());
+  return BFB_OK;
+}
+
+}  // namespace
+
+// One rank's share (SURVEY §8 e: GPU g owns offsets[b[g]..b[g+1]] and that
+// adjacency slice).  partition_1d needs every vertex's deduplicated degree,
+// so the rows are first built slice by slice under a bounded edge budget
+// (degrees kept, adjacency dropped), then the offsets and the partition are
+// computed, and the owned rows are built once more and kept.  The generator
+// re-runs per slice instead of storing the edge list (PCG64 jump-ahead).
+int build_from_rmat_part(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc,
+                         const uint64_t thr[3], int parts, int rank, int64_t* bounds_out) {
+  BFB_TRY(check_rmat_args(scale, ef));
+  if (parts < 1 || rank < 0 || rank >= parts) return fail(BFB_ERR_INVALID, "bad parts / rank");
+  RmatParams P = make_params(scale, ef, state, inc, thr);
+  const int64_t n = int64_t(1) << scale;
+  if (parts > n) return fail(BFB_ERR_INVALID, "num_parts exceeds the number of vertices");
+  engine_release(ctx);
+  relabel_release(ctx);
+  ctx->g = DevGraph();
+  cudaStream_t s = ctx->stream;
+  const int sms = ctx->num_sms;
+  DevBuf<uint32_t> deg, ddeg;
+  BFB_TRY(deg.alloc(n));
+  BFB_TRY(ddeg.alloc(n));
+  BFB_CUDA(cudaMemsetAsync(deg.p, 0, n * sizeof(uint32_t), s));
+  BuildSink sink{};
+  sink.deg = deg.p;
+  BFB_TRY(launch_rmat<kModeCount>(P, sink, s));
+  // degree pass: slices of <= kBudget raw (pre-dedup) entries
+  const int64_t kBudget = int64_t(1) << 31;
+  int64_t raw_total = 0;
+  std::vector<int64_t> cuts;
+  {
+    DevBuf<int64_t> rs, tmp, b;
+    BFB_TRY(rs.alloc(n + 1));
+    BFB_TRY(tmp.alloc(scan_tmp_words(n) + 1));
+    BFB_TRY(scan_u32_to_i64(deg.p, n, rs.p, tmp.p, s));
+    BFB_CUDA(cudaMemcpyAsync(&raw_total, rs.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
+    const int ns = (int)std::max<int64_t>(1, (raw_total + kBudget - 1) / kBudget);
+    BFB_TRY(b.alloc(ns + 1));
+    k_partition<<<(ns + 1 + 127) / 128, 128, 0, s>>>(rs.p, n, raw_total, ns, b.p);
+    cuts.resize(ns + 1);
+    BFB_CUDA(cudaMemcpyAsync(cuts.data(), b.p, (ns + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
+  }
+  for (size_t k = 0; k + 1 < cuts.size(); ++k)
+    BFB_TRY(rmat_slice(ctx, P, deg.p, cuts[k], cuts[k + 1], ddeg.p, nullptr));
+  // offsets of the whole graph, max degree, the partition
+  DevGraph G;
+  G.n = n;
+  BFB_TRY(G.offsets.alloc(n + 1));
+  {
+    DevBuf<int64_t> tmp;
+    BFB_TRY(tmp.alloc(scan_tmp_words(n) + 1));
+    BFB_TRY(scan_u32_to_i64(ddeg.p, n, G.offsets.p, tmp.p, s));
+  }
+  DevBuf<unsigned long long> maxdeg;
+  BFB_TRY(maxdeg.alloc(1));
+  BFB_CUDA(cudaMemsetAsync(maxdeg.p, 0, sizeof(unsigned long long), s));
+  k_max_degree<<<grid_for(n, 256, sms), 256, 0, s>>>(G.offsets.p, n, maxdeg.p);
+  unsigned long long md = 0;
+  BFB_CUDA(cudaMemcpyAsync(&G.m, G.offsets.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  BFB_CUDA(cudaMemcpyAsync(&md, maxdeg.p, sizeof(md), cudaMemcpyDeviceToHost, s));
+  std::vector<int64_t> b(parts + 1);
+  {
+    DevBuf<int64_t> bd;
+    BFB_TRY(bd.alloc(parts + 1));
+    BFB_CUDA(cudaStreamSynchronize(s));
+    k_partition<<<(parts + 1 + 127) / 128, 128, 0, s>>>(G.offsets.p, n, G.m, parts, bd.p);
+    BFB_CUDA(cudaMemcpyAsync(b.data(), bd.p, (parts + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
+  }
+  G.max_degree = (int64_t)md;
+  // the owned rows, kept
+  G.row_lo = b[rank];
+  G.row_hi = b[rank + 1];
+  BFB_CUDA(cudaMemcpy(&G.adj_lo, G.offsets.p + G.row_lo, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (G.row_hi > G.row_lo) {
+    BFB_TRY(rmat_slice(ctx, P, deg.p, G.row_lo, G.row_hi, ddeg.p, &G.adj));
+  } else {
+    BFB_TRY(G.adj.alloc(1));
+  }
+  G.valid = true;
+  ctx->g = std::move(G);
+  if (bounds_out) std::copy(b.begin(), b.end(), bounds_out);
+  return BFB_OK;
+}
 
 int rmat_to_host(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc, const uint64_t thr[3],
                  uint32_t* out) {
@@ -508,6 +627,7 @@ int build_from_rmat(bfb_ctx* ctx, int scale, int64_t ef, U128 state, U128 inc,
   RmatParams P = make_params(scale, ef, state, inc, thr);
   int64_t n = int64_t(1) << scale;
   engine_release(ctx);
+  relabel_release(ctx);
   ctx->g = DevGraph();  // free the previous graph before the big allocations
   DevBuf<uint32_t> deg;
   BFB_TRY(deg.alloc(n));
@@ -526,6 +646,7 @@ int build_from_edges(bfb_ctx* ctx, int64_t n, const uint32_t* host_edges, int64_
   if (n < 0 || m < 0) return fail(BFB_ERR_INVALID, "negative size");
   if (n > (int64_t(1) << 32)) return fail(BFB_ERR_INVALID, "num_vertices exceeds the VID range");
   engine_release(ctx);
+  relabel_release(ctx);
   ctx->g = DevGraph();
   DevBuf<uint2> edges;
   BFB_TRY(edges.alloc(m));
@@ -541,6 +662,7 @@ int build_from_device_edges(bfb_ctx* ctx, int64_t n, DevBuf<uint2>& edges, int64
   if (n < 0 || m < 0) return fail(BFB_ERR_INVALID, "negative size");
   if (n > (int64_t(1) << 32)) return fail(BFB_ERR_INVALID, "num_vertices exceeds the VID range");
   engine_release(ctx);
+  relabel_release(ctx);
   ctx->g = DevGraph();
   cudaStream_t s = ctx->stream;
   DevBuf<uint32_t> deg;
@@ -573,6 +695,7 @@ int build_from_device_edges(bfb_ctx* ctx, int64_t n, DevBuf<uint2>& edges, int64
 int load_csr(bfb_ctx* ctx, int64_t n, int64_t m, const int64_t* offsets, const uint32_t* adj) {
   if (n < 0 || m < 0) return fail(BFB_ERR_INVALID, "negative size");
   engine_release(ctx);
+  relabel_release(ctx);
   ctx->g = DevGraph();
   DevBuf<int64_t> off;
   DevBuf<uint32_t> a;
@@ -593,6 +716,9 @@ int load_csr(bfb_ctx* ctx, int64_t n, int64_t m, const int64_t* offsets, const u
   ctx->g.n = n;
   ctx->g.m = m;
   ctx->g.max_degree = (int64_t)md;
+  ctx->g.row_lo = 0;
+  ctx->g.row_hi = n;
+  ctx->g.adj_lo = 0;
   ctx->g.valid = true;
   return BFB_OK;
 }
