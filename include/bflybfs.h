@@ -106,11 +106,22 @@ int bfb_message_count_paper(int num_nodes, int fanout, int64_t* out);
 /* buffer_bound */
 int64_t bfb_buffer_bound(int64_t num_vertices, int fanout);
 
+/* Allocation tracking (SPEC.md acceptance 4): device and pinned-host
+ * allocations the library has made so far; equal before and after a
+ * bfb_bfs / bfb_rank_bfs call, read-out included (allocation-freedom). */
+int64_t bfb_alloc_count(void);
+
 /* ---- context ----------------------------------------------------------- */
 int bfb_create(bfb_ctx** ctx_out, int device);
 void bfb_destroy(bfb_ctx* ctx);
 /* Record per-phase CUDA events inside bfb_bfs (fills *_ms of bfb_run_stats). */
 int bfb_set_timing(bfb_ctx* ctx, int enabled);
+/* Instrumentation (SPEC.md acceptance 8): flags 1 = after every phase 2,
+ * check that all nodes' visited bitmaps (levels so far + the synchronized
+ * frontier) are identical; bfb_bfs then fails with BFB_ERR_CAPACITY on a
+ * disagreement.  (Rank mode always all-reduces and checks the per-level
+ * frontier count.)  0 = off (default). */
+int bfb_set_checks(bfb_ctx* ctx, int flags);
 /* Phase-1 direction (paper contribution 3; SPEC.md:172 keeps
  * the slot): 0 = top-down (Alg. 2, default), 1 = direction-optimizing with
  * Beamer's switch (TD->BU when frontier edges > unexplored edges / alpha,
@@ -167,6 +178,23 @@ int bfb_graph_from_rmat(bfb_ctx* ctx, int scale, int64_t edge_factor,
  * 2*m uint32 host values (src, dst) pairs; the CSR stays resident in ctx. */
 int bfb_graph_from_edges(bfb_ctx* ctx, int64_t num_vertices, const uint32_t* edges, int64_t m,
                          int symmetrize);
+/* One rank's share of the generate_rmat -> symmetrize -> build_csr graph
+ * (SURVEY §8 e: GPU g owns offsets[b[g]..b[g+1]] and that adjacency slice):
+ * the context keeps the whole offsets (every vertex's degree) and only the
+ * adjacency of rows [b[rank], b[rank+1]) of partition_1d(num_parts) of the
+ * final graph, whose num_parts+1 boundaries go to boundaries_out.  Rows are
+ * built slice by slice under a bounded edge budget (the generator re-runs
+ * per slice), so a rank never holds the whole edge set.  Such a context runs
+ * bfb_rank_setup for that rank; whole-graph calls (CSR / edge copies, save,
+ * bfb_engine_setup, certificates) return BFB_ERR_STATE. */
+int bfb_graph_from_rmat_part(bfb_ctx* ctx, int scale, int64_t edge_factor,
+                             const uint64_t pcg_state[2], const uint64_t pcg_inc[2],
+                             const uint64_t thresholds[3], int num_parts, int rank,
+                             int64_t* boundaries_out);
+/* Rows whose adjacency this context holds ([0, n) unless partitioned) and
+ * the number of adjacency entries resident. */
+int bfb_graph_rows(bfb_ctx* ctx, int64_t* row_lo_out, int64_t* row_hi_out,
+                   int64_t* adjacency_entries_out);
 /* Upload an existing CSR (reference Graph, graphs.py:53-64). */
 int bfb_graph_load_csr(bfb_ctx* ctx, int64_t num_vertices, int64_t num_edges,
                        const int64_t* offsets, const uint32_t* adjacency);

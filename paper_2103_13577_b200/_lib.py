@@ -80,6 +80,8 @@ _SIGNATURES = {
     "bfb_num_rounds": (c_int, [c_int, c_int, POINTER(c_int)]),
     "bfb_make_schedule": (c_int, [c_int, c_int, c_int, _I32P, c_int64, _I64P]),
     "bfb_message_count_paper": (c_int, [c_int, c_int, _I64P]),
+    "bfb_alloc_count": (c_int64, []),
+    "bfb_set_checks": (c_int, [c_void_p, c_int]),
     "bfb_buffer_bound": (c_int64, [c_int64, c_int]),
     "bfb_create": (c_int, [POINTER(c_void_p), c_int]),
     "bfb_destroy": (None, [c_void_p]),
@@ -89,6 +91,9 @@ _SIGNATURES = {
     "bfb_timer_stop": (c_int, [c_void_p, POINTER(c_double)]),
     "bfb_rmat_edges": (c_int, [c_void_p, c_int, c_int64, _U64P, _U64P, _U64P, _U32P]),
     "bfb_graph_from_rmat": (c_int, [c_void_p, c_int, c_int64, _U64P, _U64P, _U64P]),
+    "bfb_graph_from_rmat_part": (c_int, [c_void_p, c_int, c_int64, _U64P, _U64P, _U64P, c_int,
+                                         c_int, _I64P]),
+    "bfb_graph_rows": (c_int, [c_void_p, _I64P, _I64P, _I64P]),
     "bfb_graph_from_edges": (c_int, [c_void_p, c_int64, _U32P, c_int64, c_int]),
     "bfb_graph_load_csr": (c_int, [c_void_p, c_int64, c_int64, _I64P, _U32P]),
     "bfb_graph_info": (c_int, [c_void_p, _I64P, _I64P, _I64P]),

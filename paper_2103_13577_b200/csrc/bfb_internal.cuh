@@ -31,7 +31,10 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 
 // ------------------------------------------------------- device buffers --
 // Owning device allocation.  All engine buffers are created in setup calls;
-// bfb_bfs itself never allocates.
+// bfb_bfs itself never allocates -- every
+// device and pinned-host allocation of the library bumps alloc_counter(),
+// which the allocation-freedom test reads around bfb_bfs (bfb_alloc_count).
+int64_t& alloc_counter();
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -48,6 +51,7 @@ struct DevBuf {
   int alloc(size_t count) {
     release();
     if (count == 0) count = 1;
+    ++alloc_counter();
     cudaError_t e = cudaMalloc(&p, count * sizeof(T));
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -172,6 +176,7 @@ struct RunCounters {
   int64_t traversed_edges;
   int64_t reached;
   int64_t exchange_bytes;
+  int64_t disagree;        // checks mode: words where a node's frontier differs from node 0's
 };
 
 // One compute node's private world (NodeState).
@@ -202,6 +207,8 @@ struct Part {
 
 namespace bfb {
 struct EngineTables;  // bfs_engine.cu: device-side pointer/schedule tables
+
+struct ReadPool;  // host_out.cu: persistent widening threads of the read-out
 
 // Result read-out (host_out.cu): a page-locked staging area for the packed
 // D2H copy and one event per pipelined chunk.
@@ -241,6 +248,7 @@ struct bfb_ctx {
   bfb::EngineTables* tables = nullptr;
   int expand_grid = 0;
   bool timing = false;
+  int checks = 0;                     // bfb_set_checks: 1 = frontier agreement after phase 2
   int direction = 0;                  // 0 top-down, 1 direction-optimizing, 2 bottom-up
   double do_alpha = 5.0, do_beta = 1024.0;  // tuned at s29 (Beamer: 14, 24)
   bool have_run = false;
@@ -255,6 +263,7 @@ struct bfb_ctx {
   // result read-out: packed levels on device, staging in host memory
   bfb::DevBuf<uint32_t> packed;
   bfb::HostStage stage;
+  bfb::ReadPool* pool = nullptr;
   // the engine's degree-ordered relabel of the graph (relabel.cu), kept
   // across engine setups with the same partition: eg = relabelled CSR,
   // perm = old -> new id, inv = new -> old id; results are mapped back to
@@ -297,6 +306,10 @@ int count_nonisolated(bfb_ctx* ctx, int64_t* out);
 int read_levels(bfb_ctx* ctx, const uint32_t* level, int64_t n, int64_t num_levels,
                 uint32_t* out, cudaStream_t s);
 int read_parents(bfb_ctx* ctx, const uint32_t* parent, int64_t n, int64_t* out, cudaStream_t s);
+// the read-out's buffers (packed levels, pinned stage, events, host threads),
+// allocated at engine setup so bfb_bfs allocates nothing
+int readout_setup(bfb_ctx* ctx, int64_t n);
+void readout_release(bfb_ctx* ctx);
 int select_nonisolated(bfb_ctx* ctx, const int64_t* ranks, int64_t k, int64_t* out);
 
 // relabel.cu: the engine's degree-ordered relabel (within the parts of `bounds`)
@@ -304,9 +317,9 @@ bool relabel_wanted(const bfb_ctx* ctx);
 int relabel_build(bfb_ctx* ctx, const std::vector<int64_t>& bounds);
 void relabel_release(bfb_ctx* ctx);
 // segsort.cu: per-row ascending sort of rows[rowstart[v]..rowstart[v+1]) into
-// out (hand-written warp bitonic / block radix); clobbers rows
+// out (hand-written warp bitonic / block radix); keys < key_bound; clobbers rows
 int sort_rows(bfb_ctx* ctx, const int64_t* rowstart, int64_t n, int64_t total, uint32_t* rows,
-              uint32_t* out);
+              uint32_t* out, int64_t key_bound);
 
 // scan.cu: exclusive scan of n values produced by a loader -> int64 out[0..n]
 // (out[n] = total).  Work buffers are sized by the caller via scan_tmp_words.

@@ -497,6 +497,20 @@ __global__ void k_merge(RoundDesc rd, uint32_t* const* pubs, uint32_t* const* vi
   }
 }
 
+// Checks mode (SPEC.md acceptance 8, frontier agreement): after phase 2 every
+// node's visited bitmap -- levels <= L plus the synchronized frontier -- must
+// equal node 0's; counts the words that differ.
+__global__ void k_agree(uint32_t* const* visiteds, int num_nodes, int64_t nwords,
+                        RunCounters* run) {
+  unsigned long long bad = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = visiteds[0][w];
+    for (int g = 1; g < num_nodes; ++g) bad += visiteds[g][w] != a;
+  }
+  if (bad) atomicAdd((unsigned long long*)&run->disagree, bad);
+}
+
 // ------------------------------------------------------------- commit ----
 __global__ void k_commit_prep(PartCounters** ctrs, int num_nodes) {
   for (int g = threadIdx.x; g < num_nodes; g += blockDim.x) {
@@ -1766,6 +1780,7 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
   else
     BFB_TRY(expand_occupancy<false>(&occ));
   ctx->expand_grid = std::max(1, occ) * ctx->num_sms;
+  BFB_TRY(readout_setup(ctx, n));  // read-out buffers: bfb_bfs allocates nothing
   for (auto& ev : D->ev) BFB_CUDA(cudaEventCreate(&ev));
   if (parts > 1) {
     D->part_ev.resize(parts + 1);
@@ -1885,6 +1900,10 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
         k_merge<<<grid, 256, 0, s>>>(rd, D->pubs.p, D->visiteds.p, D->ctrs.p, parity, nwords);
         ++launches;
       }
+    }
+    if (ctx->checks & 1 && P > 1) {
+      k_agree<<<grid_cap(nwords, 256, sms, 2), 256, 0, s>>>(D->visiteds.p, P, nwords, ctx->run.p);
+      ++launches;
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[4], s));
     // Commit: levels, start snapshot, next q_local, frontier count.
@@ -2052,6 +2071,9 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     st->expand_max_part_ms = t_expand_max;
     st->switch_checksum = switch_chk;
   }
+  if (rc.disagree)
+    return fail(BFB_ERR_CAPACITY, "frontier disagreement after phase 2 (" +
+                                      std::to_string(rc.disagree) + " bitmap words differ)");
   // buffer-bound check: incoming <= f * |V|
   for (auto x : hw)
     if (x > (int64_t)ctx->fanout * n && ctx->strategy == BFB_STRATEGY_BUTTERFLY)
@@ -2210,6 +2232,7 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   if (want_parents) {
     D->peer_parent[rank] = p.parent.p;
     BFB_TRY(D->parents_final.alloc(n + 1));
+    BFB_TRY(D->parents.alloc(parts));  // peers' parent pointers (rank_parents)
   }
   D->seq = 0;
   if (ctx->direction) BFB_CUDA(cudaMemset(p.front.p, 0, nwords_pad * sizeof(uint32_t)));
@@ -2412,7 +2435,6 @@ int rank_parents(bfb_ctx* ctx, int64_t* out) {
   const int P = ctx->num_parts;
   for (int g = 0; g < P; ++g)
     if (!D->peer_parent[g]) return fail(BFB_ERR_STATE, "peer parents not mapped");
-  if (D->parents.n < (size_t)P) BFB_TRY(D->parents.alloc(P));
   BFB_CUDA(cudaMemcpy(D->parents.p, D->peer_parent.data(), P * sizeof(uint32_t*),
                       cudaMemcpyHostToDevice));
   const int64_t n = ctx->g.n;
@@ -2493,11 +2515,34 @@ __global__ void k_wait(const int64_t* mail, int me, int num_nodes, int64_t seq, 
   const uint64_t t0 = globaltimer_ns();
   while (ld_acquire_sys(mail + kMail * g + 2) < seq) {
     if (globaltimer_ns() - t0 > timeout_ns) {
-      atomicExch(err, 1);
+      atomicOr(err, 1);
       return;
     }
     __nanosleep(200);
   }
+}
+
+// Termination all-reduce (the north star's per-level frontier
+// count reduction) over the same mailboxes: every node writes its owned share
+// of the next frontier (slot 3) and the barrier seq into every peer's
+// mailbox; after the barrier each node sums the shares and checks the sum
+// against the frontier it committed itself (err bit 2 on disagreement).
+__global__ void k_signal_count(int64_t* const* peer_mail, int me, int num_nodes, int64_t seq,
+                               const PartCounters* ctr) {
+  const int g = threadIdx.x;
+  if (g >= num_nodes || g == me) return;
+  int64_t* slot = peer_mail[g] + kMail * me;
+  slot[3] = ((volatile const PartCounters*)ctr)->q_count;
+  st_release_sys(slot + 2, seq);
+}
+
+__global__ void k_check_count(const int64_t* mail, int me, int num_nodes, const PartCounters* ctr,
+                              int32_t* err) {
+  if (threadIdx.x) return;
+  int64_t sum = ctr->q_count;
+  for (int g = 0; g < num_nodes; ++g)
+    if (g != me) sum += ld_acquire_sys(mail + kMail * g + 3);
+  if (sum != ctr->frontier) atomicOr(err, 2);
 }
 
 struct RoundSrc {
@@ -2748,13 +2793,25 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
         launches += launch_commit_write(cv, off, next_level, !next_bu, sms, s);
       }
     }
+    // the level's frontier count, all-reduced over the nodes' owned shares
+    // and checked against this node's own commit
+    if (P > 1) {
+      const int64_t cseq = ++D->seq;
+      k_signal_count<<<1, 64, 0, s>>>(D->peer_mail_dev.p, me, P, cseq, p.ctr.p);
+      k_wait<<<1, 64, 0, s>>>(D->mail.p, me, P, cseq, D->err.p, timeout_ns);
+      k_check_count<<<1, 32, 0, s>>>(D->mail.p, me, P, p.ctr.p, D->err.p);
+      launches += 3;
+    }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 4, D->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaStreamSynchronize(s));
     BFB_CUDA(cudaGetLastError());
-    if (*(int32_t*)(ctx->pinned + 4))
-      return fail(BFB_ERR_CUDA, "peer barrier timed out (a rank stopped participating)");
+    const int32_t errs = *(int32_t*)(ctx->pinned + 4);
+    if (errs & 1) return fail(BFB_ERR_CUDA, "peer barrier timed out (a rank stopped participating)");
+    if (errs & 2)
+      return fail(BFB_ERR_CAPACITY, "frontier disagreement: the nodes' owned shares do not sum "
+                                    "to the committed frontier");
     if (ctx->timing) {
       float a = 0, b = 0, c = 0;
       BFB_CUDA(cudaEventElapsedTime(&a, D->ev[2], D->ev[3]));

@@ -9,6 +9,11 @@ namespace bfb {
 
 static thread_local std::string tl_error;
 
+int64_t& alloc_counter() {
+  static int64_t count = 0;  // bumped under the context mutex (or in setup-only paths)
+  return count;
+}
+
 void set_error(const std::string& msg) { tl_error = msg; }
 
 int fail(int code, const std::string& msg) {
@@ -79,6 +84,9 @@ using namespace bfb;
 
 #define NEED_GRAPH(ctx) \
   if (!(ctx)->g.valid) return fail(BFB_ERR_STATE, "no graph loaded")
+#define NEED_FULL_GRAPH(ctx)  \
+  if (!(ctx)->g.full())       \
+  return fail(BFB_ERR_STATE, "this context holds one rank's rows only (partitioned build)")
 
 // The single-context entry points (bfb_bfs and its read-outs) index every
 // node's buffers; after bfb_rank_setup the context holds one node only.
@@ -159,6 +167,8 @@ int bfb_message_count_paper(int num_nodes, int fanout, int64_t* out) {
 
 int64_t bfb_buffer_bound(int64_t num_vertices, int fanout) { return (int64_t)fanout * num_vertices; }
 
+int64_t bfb_alloc_count(void) { return alloc_counter(); }
+
 int bfb_create(bfb_ctx** ctx_out, int device) {
   if (!ctx_out) return fail(BFB_ERR_INVALID, "null output");
   *ctx_out = nullptr;
@@ -190,6 +200,7 @@ void bfb_destroy(bfb_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   engine_release(ctx);
   relabel_release(ctx);
+  readout_release(ctx);
   ctx->g = DevGraph();
   for (auto& e : ctx->timer)
     if (e) cudaEventDestroy(e);
@@ -200,6 +211,13 @@ void bfb_destroy(bfb_ctx* ctx) {
 int bfb_set_timing(bfb_ctx* ctx, int enabled) {
   CTX_GUARD(ctx);
   ctx->timing = enabled != 0;
+  return BFB_OK;
+}
+
+int bfb_set_checks(bfb_ctx* ctx, int flags) {
+  CTX_GUARD(ctx);
+  if (flags < 0 || flags > 1) return fail(BFB_ERR_INVALID, "unknown check flags");
+  ctx->checks = flags;
   return BFB_OK;
 }
 
@@ -253,6 +271,27 @@ int bfb_graph_from_rmat(bfb_ctx* ctx, int scale, int64_t edge_factor, const uint
                          thresholds);
 }
 
+int bfb_graph_from_rmat_part(bfb_ctx* ctx, int scale, int64_t edge_factor,
+                             const uint64_t pcg_state[2], const uint64_t pcg_inc[2],
+                             const uint64_t thresholds[3], int num_parts, int rank,
+                             int64_t* boundaries_out) {
+  CTX_GUARD(ctx);
+  if (!pcg_state || !pcg_inc || !thresholds || !boundaries_out)
+    return fail(BFB_ERR_INVALID, "null argument");
+  return build_from_rmat_part(ctx, scale, edge_factor, u128_of(pcg_state), u128_of(pcg_inc),
+                              thresholds, num_parts, rank, boundaries_out);
+}
+
+int bfb_graph_rows(bfb_ctx* ctx, int64_t* row_lo_out, int64_t* row_hi_out,
+                   int64_t* adjacency_entries_out) {
+  CTX_GUARD(ctx);
+  NEED_GRAPH(ctx);
+  if (row_lo_out) *row_lo_out = ctx->g.row_lo;
+  if (row_hi_out) *row_hi_out = ctx->g.row_hi;
+  if (adjacency_entries_out) *adjacency_entries_out = ctx->g.full() ? ctx->g.m : (int64_t)ctx->g.adj.n - 1;
+  return BFB_OK;
+}
+
 int bfb_graph_from_edges(bfb_ctx* ctx, int64_t num_vertices, const uint32_t* edges, int64_t m,
                          int symmetrize) {
   CTX_GUARD(ctx);
@@ -281,6 +320,7 @@ int bfb_graph_info(bfb_ctx* ctx, int64_t* n, int64_t* m, int64_t* maxdeg) {
 int bfb_graph_copy_csr(bfb_ctx* ctx, int64_t* offsets_out, uint32_t* adjacency_out) {
   CTX_GUARD(ctx);
   NEED_GRAPH(ctx);
+  if (adjacency_out) NEED_FULL_GRAPH(ctx);
   if (offsets_out)
     BFB_CUDA(cudaMemcpy(offsets_out, ctx->g.offsets.p, (ctx->g.n + 1) * sizeof(int64_t),
                         cudaMemcpyDeviceToHost));
@@ -293,6 +333,7 @@ int bfb_graph_copy_csr(bfb_ctx* ctx, int64_t* offsets_out, uint32_t* adjacency_o
 int bfb_graph_copy_edges(bfb_ctx* ctx, uint32_t* edges_out) {
   CTX_GUARD(ctx);
   NEED_GRAPH(ctx);
+  NEED_FULL_GRAPH(ctx);
   if (!edges_out && ctx->g.m) return fail(BFB_ERR_INVALID, "null output");
   return copy_edges(ctx, edges_out);
 }
@@ -399,6 +440,8 @@ int bfb_write_edge_list(const char* path, const uint32_t* edges, int64_t num_edg
 
 int bfb_graph_save(bfb_ctx* ctx, const char* path) {
   CTX_GUARD(ctx);
+  NEED_GRAPH(ctx);
+  NEED_FULL_GRAPH(ctx);
   if (!path) return fail(BFB_ERR_INVALID, "null path");
   return graph_save(ctx, path);
 }

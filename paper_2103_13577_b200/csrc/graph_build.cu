@@ -367,7 +367,7 @@ int finish_build(bfb_ctx* ctx, int64_t n, DevBuf<uint32_t>& deg, ScatterFn scatt
   deg.release();
   DevBuf<uint32_t> sorted;
   BFB_TRY(sorted.alloc(total));
-  BFB_TRY(sort_rows(ctx, rowstart.p, n, total, rows.p, sorted.p));
+  BFB_TRY(sort_rows(ctx, rowstart.p, n, total, rows.p, sorted.p, n));
   DevBuf<unsigned> err;
   BFB_TRY(err.alloc(1));
   BFB_CUDA(cudaMemsetAsync(err.p, 0, sizeof(unsigned), s));
@@ -482,7 +482,7 @@ int rmat_slice(bfb_ctx* ctx, const RmatParams& P, const uint32_t* deg, int64_t a
   BFB_TRY(launch_rmat<kModeScatter>(P, sink, s));
   fill.release();
   BFB_TRY(sorted.alloc(total + 1));
-  BFB_TRY(sort_rows(ctx, rowstart.p, ns, total, rows.p, sorted.p));
+  BFB_TRY(sort_rows(ctx, rowstart.p, ns, total, rows.p, sorted.p, int64_t(1) << P.scale));
   const int64_t nwords = (total + 31) / 32;
   DevBuf<uint32_t> rs_bits, keep;
   DevBuf<unsigned> err;

@@ -15,8 +15,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <thread>
 
@@ -141,12 +143,72 @@ void widen_parents(const uint32_t* in, int64_t e0, int64_t e1, int64_t* out) {
   for (; e < e1; ++e) one(e);
 }
 
+}  // namespace
+
+// Host threads that widen the landed chunks: created once at engine setup
+// and parked on a condition variable between read-outs (no thread creation
+// per call); the calling thread takes part as worker size() - 1.
+struct ReadPool {
+  std::vector<std::thread> th;
+  std::mutex mu;
+  std::condition_variable go, done;
+  std::function<void(int)> job;
+  int64_t gen = 0;
+  int pending = 0;
+  bool stop = false;
+  explicit ReadPool(int T, int dev) {
+    for (int t = 0; t + 1 < T; ++t)
+      th.emplace_back([this, t, dev] {
+        cudaSetDevice(dev);
+        int64_t seen = 0;
+        while (true) {
+          std::function<void(int)> j;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            go.wait(lk, [&] { return stop || gen != seen; });
+            if (stop) return;
+            seen = gen;
+            j = job;
+          }
+          j(t);
+          std::lock_guard<std::mutex> lk(mu);
+          if (--pending == 0) done.notify_one();
+        }
+      });
+  }
+  ~ReadPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    go.notify_all();
+    for (auto& t : th) t.join();
+  }
+  int size() const { return (int)th.size() + 1; }
+  template <class F>
+  void run(F& f) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      job = [&f](int t) { f(t); };
+      pending = (int)th.size();
+      ++gen;
+    }
+    go.notify_all();
+    f((int)th.size());
+    std::unique_lock<std::mutex> lk(mu);
+    done.wait(lk, [&] { return pending == 0; });
+  }
+};
+
+namespace {
+
 int ensure_stage(bfb_ctx* ctx, size_t bytes, int nchunks) {
   HostStage& st = ctx->stage;
   if (st.bytes < bytes) {
     if (st.p) cudaFreeHost(st.p);
     st.p = nullptr;
     st.bytes = 0;
+    ++alloc_counter();
     BFB_CUDA(cudaHostAlloc(&st.p, bytes, cudaHostAllocDefault));
     st.bytes = bytes;
   }
@@ -176,11 +238,9 @@ int pipelined_read(bfb_ctx* ctx, const void* src, size_t bytes, cudaStream_t s, 
                              cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaEventRecord(ctx->stage.ev[k], s));
   }
-  const int T = bytes < (size_t(8) << 20) ? 1 : host_threads();
+  const int T = bytes < (size_t(8) << 20) || !ctx->pool ? 1 : ctx->pool->size();
   std::atomic<int> bad{0};
-  const int dev = ctx->device;
   auto run = [&](int t) {
-    if (T > 1) cudaSetDevice(dev);
     for (int k = 0; k < nchunks; ++k) {
       if (cudaEventSynchronize(ctx->stage.ev[k]) != cudaSuccess) {
         bad.store(1);
@@ -193,20 +253,33 @@ int pipelined_read(bfb_ctx* ctx, const void* src, size_t bytes, cudaStream_t s, 
     }
     _mm_sfence();
   };
-  if (T == 1) {
+  if (T == 1)
     run(0);
-  } else {
-    std::vector<std::thread> pool;
-    pool.reserve(T - 1);
-    for (int t = 0; t + 1 < T; ++t) pool.emplace_back(run, t);
-    run(T - 1);
-    for (auto& th : pool) th.join();
-  }
+  else
+    ctx->pool->run(run);
   if (bad.load()) BFB_CUDA(cudaStreamSynchronize(s));
   return BFB_OK;
 }
 
 }  // namespace
+
+int readout_setup(bfb_ctx* ctx, int64_t n) {
+  if (n <= 0) return BFB_OK;
+  // packed levels: 8 bits per vertex at most; stage: a uint32 per vertex
+  // (parents, or levels past 255); one event per chunk (<= 32 + 1 chunks)
+  const int64_t words = (n + 3) / 4;
+  if ((int64_t)ctx->packed.n < words) BFB_TRY(ctx->packed.alloc((size_t)words));
+  BFB_TRY(ensure_stage(ctx, (size_t)n * 4, 40));
+  if (!ctx->pool) ctx->pool = new ReadPool(host_threads(), ctx->device);
+  return BFB_OK;
+}
+
+void readout_release(bfb_ctx* ctx) {
+  delete ctx->pool;
+  ctx->pool = nullptr;
+  ctx->packed.release();
+  ctx->stage.release();
+}
 
 int read_levels(bfb_ctx* ctx, const uint32_t* level, int64_t n, int64_t num_levels,
                 uint32_t* out, cudaStream_t s) {

@@ -75,6 +75,13 @@ __global__ void __launch_bounds__(kRelabelBlock) k_class_scatter(const int64_t* 
   }
 }
 
+__global__ void k_rel_offsets(const int64_t* __restrict__ noff, int64_t lo, int64_t cnt,
+                              int64_t* rel) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    rel[i] = noff[lo + i] - noff[lo];
+}
+
 __global__ void k_new_degrees(const int64_t* __restrict__ off, const uint32_t* __restrict__ inv,
                               int64_t n, uint32_t* deg) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
@@ -91,17 +98,19 @@ __global__ void __launch_bounds__(256) k_gather_rows(const int64_t* __restrict__
                                                      const uint32_t* __restrict__ adj,
                                                      const int64_t* __restrict__ noff,
                                                      const uint32_t* __restrict__ perm,
-                                                     const uint32_t* __restrict__ inv, int64_t n,
-                                                     unsigned long long* next, uint32_t* out) {
+                                                     const uint32_t* __restrict__ inv, int64_t r_lo,
+                                                     int64_t r_hi, unsigned long long* next,
+                                                     uint32_t* out) {
   const int lane = threadIdx.x & 31;
+  const int64_t obase = noff[r_lo];
   while (true) {
-    unsigned long long r = 0;
-    if (lane == 0) r = atomicAdd(next, 1ull);
-    r = __shfl_sync(0xffffffffu, r, 0);
-    if ((int64_t)r >= n) return;
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(next, 1ull);
+    const int64_t r = r_lo + (int64_t)__shfl_sync(0xffffffffu, k, 0);
+    if (r >= r_hi) return;
     const uint32_t v = __ldg(inv + r);
     const int64_t b = __ldg(off + v), d = __ldg(off + v + 1) - b;
-    const int64_t o = __ldg(noff + r);
+    const int64_t o = __ldg(noff + r) - obase;
     for (int64_t j0 = 0; j0 < d; j0 += 32 * 8) {
       uint32_t u[8];
 #pragma unroll
@@ -174,15 +183,27 @@ int relabel_build(bfb_ctx* ctx, const std::vector<int64_t>& bounds) {
     BFB_CUDA(cudaStreamSynchronize(s));
   }
   {
+    // the rows this context holds (all of them, or one rank's part: the
+    // relabel maps each part onto itself, so the part's rows stay its own)
+    const int64_t lo = ctx->g.row_lo, hi = ctx->g.row_hi;
+    eg.row_lo = lo;
+    eg.row_hi = hi;
+    eg.adj_lo = ctx->g.adj_lo;
+    int64_t ms = 0;
+    BFB_CUDA(cudaMemcpy(&ms, eg.offsets.p + hi, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    ms -= eg.adj_lo;
     DevBuf<uint32_t> rows;
+    DevBuf<int64_t> rel;
     DevBuf<unsigned long long> next;
-    BFB_TRY(rows.alloc(m + 1));
+    BFB_TRY(rows.alloc(ms + 1));
+    BFB_TRY(rel.alloc(hi - lo + 1));
     BFB_TRY(next.alloc(1));
     BFB_CUDA(cudaMemsetAsync(next.p, 0, sizeof(unsigned long long), s));
-    k_gather_rows<<<(unsigned)sms * 8, 256, 0, s>>>(off, ctx->g.adj.p, eg.offsets.p, ctx->perm.p,
-                                                    ctx->inv.p, n, next.p, rows.p);
-    BFB_TRY(eg.adj.alloc(m + 1));
-    BFB_TRY(sort_rows(ctx, eg.offsets.p, n, m, rows.p, eg.adj.p));
+    k_gather_rows<<<(unsigned)sms * 8, 256, 0, s>>>(off, ctx->g.adj_index(), eg.offsets.p,
+                                                    ctx->perm.p, ctx->inv.p, lo, hi, next.p, rows.p);
+    k_rel_offsets<<<grid_of(hi - lo + 1, 256, sms), 256, 0, s>>>(eg.offsets.p, lo, hi - lo, rel.p);
+    BFB_TRY(eg.adj.alloc(ms + 1));
+    BFB_TRY(sort_rows(ctx, rel.p, hi - lo, ms, rows.p, eg.adj.p, n));
     BFB_CUDA(cudaStreamSynchronize(s));
   }
   BFB_CUDA(cudaGetLastError());

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kRadixBlock) k_sort_rows_radix(const int64_t* 
 }  // namespace
 
 int sort_rows(bfb_ctx* ctx, const int64_t* rowstart, int64_t n, int64_t total, uint32_t* rows,
-              uint32_t* out) {
+              uint32_t* out, int64_t key_bound) {
   if (n <= 0 || total <= 0) return BFB_OK;
   cudaStream_t s = ctx->stream;
   const int sms = ctx->num_sms;
@@ -183,9 +183,9 @@ int sort_rows(bfb_ctx* ctx, const int64_t* rowstart, int64_t n, int64_t total, u
   const int64_t want = (n + 32 * kSortWarps - 1) / (32 * kSortWarps);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(1, occ)));
   k_sort_rows_warp<<<grid, kSortWarps * 32, 0, s>>>(rowstart, n, rows, out, big.p, nbig.p);
-  // key bits: vertex ids < n (rows hold neighbour ids of an n-vertex graph)
+  // key bits: the rows hold vertex ids < key_bound
   int bits = 1;
-  while (bits < 32 && ((int64_t)1 << bits) < n) ++bits;
+  while (bits < 32 && ((int64_t)1 << bits) < key_bound) ++bits;
   const int passes = (bits + 7) / 8;
   int occr = 1;
   BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occr, k_sort_rows_radix, kRadixBlock, 0));

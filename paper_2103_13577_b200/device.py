@@ -108,6 +108,25 @@ class DeviceGraph:
         return dg
 
     @classmethod
+    def from_rmat_part(cls, scale, edge_factor, seed, num_parts, rank, probs=None, device=0):
+        """One rank's share of the generate_rmat -> symmetrize -> build_csr
+        graph: every vertex's degree (offsets) plus the adjacency of the
+        rank's partition_1d(num_parts) rows only (``boundaries``)."""
+        from .graphs import RMAT_PROBS, rmat_device_args
+
+        state, inc, thr = rmat_device_args(scale, edge_factor, seed, probs or RMAT_PROBS)
+        dg = cls(device)
+        b = np.empty(int(num_parts) + 1, dtype=np.int64)
+        check(_lib.load().bfb_graph_from_rmat_part(dg.handle, int(scale), int(edge_factor),
+                                                   ptr(state, ctypes.c_uint64),
+                                                   ptr(inc, ctypes.c_uint64),
+                                                   ptr(thr, ctypes.c_uint64), int(num_parts),
+                                                   int(rank), ptr(b, ctypes.c_int64)))
+        dg._refresh()
+        dg.boundaries = b
+        return dg
+
+    @classmethod
     def from_edges(cls, edges, num_vertices, symmetrize, device=0):
         e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
         dg = cls(device)
@@ -144,6 +163,13 @@ class DeviceGraph:
     @property
     def max_degree(self):
         return self._maxdeg
+
+    def rows(self):
+        """(row_lo, row_hi, adjacency entries) this context holds: all rows,
+        or one rank's partition_1d share after from_rmat_part."""
+        lo, hi, m = c_int64(), c_int64(), c_int64()
+        check(_lib.load().bfb_graph_rows(self.handle, byref(lo), byref(hi), byref(m)))
+        return lo.value, hi.value, m.value
 
     def csr(self):
         off = np.empty(self._n + 1, dtype=np.int64)
@@ -225,6 +251,11 @@ class DeviceGraph:
         n, ms = c_int64(), ctypes.c_double()
         check(_lib.load().bfb_probe_peak(self.handle, int(nbytes), byref(n), byref(ms)))
         return n.value / (ms.value * 1e-3)
+
+    def set_checks(self, frontier_agreement=True):
+        """Instrumented runs (SPEC.md acceptance 8): after every phase 2 all
+        nodes' visited bitmaps must be identical, else bfs() raises."""
+        check(_lib.load().bfb_set_checks(self.handle, 1 if frontier_agreement else 0))
 
     def set_timing(self, enabled):
         check(_lib.load().bfb_set_timing(self.handle, 1 if enabled else 0))

@@ -182,6 +182,15 @@ def build_csr(el, device=0):
     return Graph(el.num_vertices, adj.size, off, adj, device=dg)
 
 
+def kronecker_part(scale, edge_factor, seed, num_parts, rank, probs=RMAT_PROBS, device=0):
+    """One rank's share of kronecker(...) for the multi-process engine
+    (SURVEY §8 e): the Graph's offsets are whole, its device adjacency holds
+    only the rows of part ``rank`` of partition_1d(num_parts) (so host
+    ``adjacency`` is unavailable).  Returns (Graph, Partition)."""
+    dg = DeviceGraph.from_rmat_part(scale, edge_factor, seed, num_parts, rank, probs, device)
+    return Graph.from_device(dg), Partition(num_parts, dg.boundaries)
+
+
 def kronecker(scale, edge_factor, seed, probs=RMAT_PROBS, device=0):
     """build_csr(symmetrize(generate_rmat(...))) entirely on device; the host
     arrays are only materialised if accessed."""

@@ -178,3 +178,84 @@ def test_rank_direction_switch_agrees_across_ranks():
             assert bus == {per_rank[0][i]["bu1"]}, a
             for r in range(world):
                 assert np.array_equal(np.load(os.path.join(out, f"lv_{r}_{i}.npy")), ref), (a, r)
+
+
+def _part_worker(rank, world, port, cases, out_dir, scale):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2103_13577_b200 import dist as bd
+    from paper_2103_13577_b200 import graphs
+
+    comm = bd.Comm()
+    g, part = graphs.kronecker_part(scale, 8, 1, world, rank, device=0)
+    dg = g.device
+    lo, hi, held = dg.rows()
+    off = g.offsets
+    info = {"lo": lo, "hi": hi, "held": held, "m": g.num_edges, "b": part.boundaries.tolist(),
+            "span": int(off[hi] - off[lo])}
+    try:  # whole-graph calls are refused on a rank's share
+        dg.csr()
+        info["csr_refused"] = False
+    except RuntimeError:
+        info["csr_refused"] = True
+    results = []
+    for fanout, strategy, root, device_sync, direction in cases:
+        eng = bd.RankEngine(dg, part.boundaries, fanout, strategy, parents=True, comm=comm,
+                            device_sync=device_sync)
+        dg.set_direction(direction)
+        d, st = eng.run(root)
+        np.save(os.path.join(out_dir, f"lv_{rank}_{len(results)}.npy"), d.d)
+        np.save(os.path.join(out_dir, f"pa_{rank}_{len(results)}.npy"), d.parents)
+        results.append({"sizes": st.per_level_frontier_size, "te": st.traversed_edges,
+                        "rm": st.remote_messages, "rv": st.remote_vertices_transferred})
+        comm.barrier()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
+        json.dump({"info": info, "results": results}, fh)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_ranks_s20_golden(golden, world):
+    """SURVEY §8 e storage: each rank builds only its share of the s20 graph
+    (every vertex's degree + its own partition_1d rows' adjacency,
+    graphs.kronecker_part) and runs the device-synchronised engine on it.
+    The shares are disjoint and cover the graph, the boundaries equal the
+    golden partition_1d, whole-graph calls are refused, and the levels match
+    the golden sha (reference graphs.py + scipy) for both directions, with
+    valid parents and RunStats equal to the lockstep oracle engine."""
+    e = golden["s20_ef8"]
+    roots = [0, e["roots64"][0]]
+    cases = [(min(2, world), "butterfly", r, True, d) for r in roots
+             for d in ("top-down", "optimizing")]
+    cases.append((1, "butterfly", roots[1], False, "top-down"))  # host-sequenced driver
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_part_worker, args=(world, _free_port(), cases, out, 20), nprocs=world,
+                           join=True, start_method="spawn")
+        per_rank = [json.load(open(os.path.join(out, f"rank{r}.json"))) for r in range(world)]
+        want_b = e["partitions"][str(world)]
+        spans = 0
+        for r in range(world):
+            info = per_rank[r]["info"]
+            assert info["b"] == want_b
+            assert (info["lo"], info["hi"]) == (want_b[r], want_b[r + 1])
+            assert info["held"] == info["span"] < info["m"]
+            assert info["csr_refused"]
+            spans += info["span"]
+        assert spans == e["num_edges"]
+        off, adj = util.rmat_graph(20)
+        for i, (f, strat, root, _, direction) in enumerate(cases):
+            want = e["bfs"][str(root)]
+            _, ost = oe.run(off, adj, np.asarray(want_b), root, fanout=f, strategy=strat)
+            for r in range(world):
+                lv = np.load(os.path.join(out, f"lv_{r}_{i}.npy"))
+                pa = np.load(os.path.join(out, f"pa_{r}_{i}.npy"))
+                res = per_rank[r]["results"][i]
+                assert util.sha16(lv) == want["levels_sha"], (world, root, direction, r)
+                assert res["sizes"] == want["sizes"] and res["te"] == want["traversed_edges"]
+                assert not ov.check_parents(off, adj, root, lv, pa)
+                if direction == "top-down":
+                    assert (res["rm"], res["rv"]) == (ost.remote_messages,
+                                                      ost.remote_vertices_transferred)
