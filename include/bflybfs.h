@@ -122,6 +122,17 @@ int bfb_set_timing(bfb_ctx* ctx, int enabled);
  * disagreement.  (Rank mode always all-reduces and checks the per-level
  * frontier count.)  0 = off (default). */
 int bfb_set_checks(bfb_ctx* ctx, int flags);
+/* Small graphs (|V| <= 2^15, |E| <= 2^21, CN <= 64, whole graph resident):
+ * top-down runs execute every level of every node inside ONE single-CTA
+ * kernel launch (no per-level launches or host round trips; deep graphs such
+ * as SPEC.md:446's path(10000) are bound by them otherwise).  Same
+ * DistanceArray, frontier sizes and RunStats counters as the level-synchronous
+ * engine, except exchange_bytes (4 B per listed vertex: list snapshots).
+ * enabled = 1 (default) uses it whenever the engine setup built its tables;
+ * 0 forces the level-synchronous engine.  Applies from the next bfb_bfs. */
+int bfb_set_small_engine(bfb_ctx* ctx, int enabled);
+/* 1 if the next top-down bfb_bfs runs on the single-CTA engine. */
+int bfb_small_engine_active(bfb_ctx* ctx);
 /* Phase-1 direction (paper contribution 3; SPEC.md:172 keeps
  * the slot): 0 = top-down (Alg. 2, default), 1 = direction-optimizing with
  * Beamer's switch (TD->BU when frontier edges > unexplored edges / alpha,

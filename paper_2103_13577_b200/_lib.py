@@ -82,6 +82,8 @@ _SIGNATURES = {
     "bfb_message_count_paper": (c_int, [c_int, c_int, _I64P]),
     "bfb_alloc_count": (c_int64, []),
     "bfb_set_checks": (c_int, [c_void_p, c_int]),
+    "bfb_set_small_engine": (c_int, [c_void_p, c_int]),
+    "bfb_small_engine_active": (c_int, [c_void_p]),
     "bfb_buffer_bound": (c_int64, [c_int64, c_int]),
     "bfb_create": (c_int, [POINTER(c_void_p), c_int]),
     "bfb_destroy": (None, [c_void_p]),

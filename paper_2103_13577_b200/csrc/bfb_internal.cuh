@@ -207,6 +207,14 @@ struct Part {
 
 namespace bfb {
 struct EngineTables;  // bfs_engine.cu: device-side pointer/schedule tables
+struct SmallEngine;   // small_bfs.cu: the single-CTA engine's tables
+
+// One single-CTA run's results (small_bfs.cu)
+struct SmallResult {
+  std::vector<int64_t> sizes;  // per_level_frontier_size
+  int64_t remote_messages = 0, remote_vertices = 0, exchange_bytes = 0, traversed_edges = 0,
+          reached = 0, disagree = 0;
+};
 
 struct ReadPool;  // host_out.cu: persistent widening threads of the read-out
 
@@ -273,6 +281,11 @@ struct bfb_ctx {
   bfb::DevGraph eg;
   bfb::DevBuf<uint32_t> perm, inv;
   bfb::DevBuf<uint32_t> out_level, out_parent;
+  // small graphs: the whole BFS in one single-CTA launch (small_bfs.cu);
+  // built at engine setup when the graph qualifies, used for top-down runs
+  // while small_mode is on (bfb_set_small_engine)
+  bfb::SmallEngine* small = nullptr;
+  int small_mode = 1;
 };
 
 namespace bfb {
@@ -320,6 +333,13 @@ void relabel_release(bfb_ctx* ctx);
 // out (hand-written warp bitonic / block radix); keys < key_bound; clobbers rows
 int sort_rows(bfb_ctx* ctx, const int64_t* rowstart, int64_t n, int64_t total, uint32_t* rows,
               uint32_t* out, int64_t key_bound);
+
+// small_bfs.cu: the single-CTA engine for small graphs
+bool small_eligible(const bfb_ctx* ctx, int parts, int total_pairs);
+int small_setup(bfb_ctx* ctx);  // after the schedule / bounds are set; no-op if not eligible
+void small_release(bfb_ctx* ctx);
+int small_bfs(bfb_ctx* ctx, int64_t root, uint32_t* level, uint32_t* parent, int64_t* high_water,
+              int checks, cudaEvent_t ev0, cudaEvent_t ev1, SmallResult* res);
 
 // scan.cu: exclusive scan of n values produced by a loader -> int64 out[0..n]
 // (out[n] = total).  Work buffers are sized by the caller via scan_tmp_words.

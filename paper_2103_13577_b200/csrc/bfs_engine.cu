@@ -1616,6 +1616,7 @@ static const uint32_t* out_levels(bfb_ctx* ctx) {
 }
 
 void engine_release(bfb_ctx* ctx) {
+  small_release(ctx);
   ctx->parts.clear();
   ctx->run.release();
   ctx->high_water.release();
@@ -1639,8 +1640,9 @@ int engine_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int
   if (parts < 1) return fail(BFB_ERR_PARTITION, "num_parts must be >= 1");
   if (ctx->g.valid && !ctx->g.full())
     return fail(BFB_ERR_STATE, "this context holds one rank's rows only (use bfb_rank_setup)");
-  return engine_setup_rb(ctx, parts, bounds, fanout, strategy, want_parents,
-                         std::vector<int64_t>(bounds, bounds + parts + 1));
+  BFB_TRY(engine_setup_rb(ctx, parts, bounds, fanout, strategy, want_parents,
+                          std::vector<int64_t>(bounds, bounds + parts + 1)));
+  return small_setup(ctx);  // small graphs: the single-CTA engine's tables too
 }
 
 static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout,
@@ -1790,6 +1792,65 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
   return BFB_OK;
 }
 
+// Small graphs (small_bfs.cu): the whole top-down run in one single-CTA
+// launch; results land in the same device buffers as engine_bfs's, so the
+// read-out, the parents view and validation are shared.
+static int small_run(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_out,
+                     int64_t* sizes_out, int64_t max_levels, int64_t* hw_out, bfb_run_stats* st) {
+  EngineTables* D = ctx->tables;
+  cudaStream_t s = ctx->stream;
+  const int P = ctx->num_parts;
+  const int64_t n = ctx->g.n;
+  uint32_t* lv = const_cast<uint32_t*>(out_levels(ctx));
+  uint32_t* par = nullptr;
+  if (ctx->want_parents)
+    par = ctx->relabeled ? ctx->out_parent.p : (P > 1 ? D->parents_final.p : ctx->parts[0].parent.p);
+  SmallResult r;
+  BFB_TRY(small_bfs(ctx, root, lv, par, ctx->high_water.p, ctx->checks & 1, D->ev[0], D->ev[1], &r));
+  const int64_t nsizes = (int64_t)r.sizes.size();
+  if (sizes_out)
+    for (int64_t i = 0; i < std::min(nsizes, max_levels); ++i) sizes_out[i] = r.sizes[i];
+  ctx->last_sizes = r.sizes;
+  std::vector<int64_t> hw(P);
+  BFB_CUDA(cudaMemcpyAsync(hw.data(), ctx->high_water.p, P * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, s));
+  if (levels_out) BFB_TRY(read_levels(ctx, lv, n, nsizes, levels_out, s));
+  BFB_CUDA(cudaStreamSynchronize(s));
+  float elapsed = 0;
+  BFB_CUDA(cudaEventElapsedTime(&elapsed, D->ev[0], D->ev[1]));
+  if (parents_out) {
+    if (!ctx->want_parents) return fail(BFB_ERR_STATE, "engine set up without parents");
+    BFB_TRY(read_parents(ctx, par, n, parents_out, s));
+    BFB_CUDA(cudaStreamSynchronize(s));
+  }
+  if (hw_out) std::memcpy(hw_out, hw.data(), P * sizeof(int64_t));
+  ctx->have_run = true;
+  ctx->last_root = root;
+  ctx->last_levels = nsizes;
+  int64_t mx = 0;
+  for (auto x : hw) mx = std::max(mx, x);
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->levels = nsizes;
+    st->rounds_executed = nsizes * (int64_t)ctx->schedule.size();
+    st->remote_messages = r.remote_messages;
+    st->remote_vertices = r.remote_vertices;
+    st->traversed_edges = r.traversed_edges;
+    st->reached = r.reached;
+    st->buffer_high_water_max = mx;
+    st->exchange_bytes = r.exchange_bytes;
+    st->elapsed_ms = elapsed;
+    st->kernel_launches = 1;
+    st->expand_launches = 1;
+  }
+  if (r.disagree)
+    return fail(BFB_ERR_CAPACITY, "frontier disagreement after phase 2 (" +
+                                      std::to_string(r.disagree) + " vertices differ)");
+  if (mx > (int64_t)ctx->fanout * n && ctx->strategy == BFB_STRATEGY_BUTTERFLY)
+    return fail(BFB_ERR_CAPACITY, "buffer bound violated");
+  return BFB_OK;
+}
+
 int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parents_out,
                int64_t* sizes_out, int64_t max_levels, int64_t* hw_out, bfb_run_stats* st) {
   if (!ctx->engine_ready) return fail(BFB_ERR_STATE, "engine not set up");
@@ -1797,6 +1858,8 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   if (root < 0 || root >= n)
     return fail(BFB_ERR_ROOT, "root " + std::to_string(root) + " out of range [0, " +
                                   std::to_string(n) + ")");
+  if (ctx->small && ctx->small_mode && ctx->direction == 0)
+    return small_run(ctx, root, levels_out, parents_out, sizes_out, max_levels, hw_out, st);
   EngineTables* D = ctx->tables;
   cudaStream_t s = ctx->stream;
   const int P = ctx->num_parts;

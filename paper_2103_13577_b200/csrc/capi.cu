@@ -221,6 +221,18 @@ int bfb_set_checks(bfb_ctx* ctx, int flags) {
   return BFB_OK;
 }
 
+int bfb_set_small_engine(bfb_ctx* ctx, int enabled) {
+  CTX_GUARD(ctx);
+  ctx->small_mode = enabled != 0;
+  return BFB_OK;
+}
+
+int bfb_small_engine_active(bfb_ctx* ctx) {
+  if (!ctx) return 0;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  return ctx->small && ctx->small_mode && ctx->direction == 0 ? 1 : 0;
+}
+
 int bfb_set_direction(bfb_ctx* ctx, int mode, double alpha, double beta) {
   CTX_GUARD(ctx);
   if (mode < 0 || mode > 2 || !(alpha > 0) || !(beta > 0))

@@ -257,6 +257,16 @@ class DeviceGraph:
         nodes' visited bitmaps must be identical, else bfs() raises."""
         check(_lib.load().bfb_set_checks(self.handle, 1 if frontier_agreement else 0))
 
+    def set_small_engine(self, enabled=True):
+        """Small graphs (|V| <= 2^15): run top-down BFSs as one single-CTA
+        launch (True, default) or force the level-synchronous engine (False)."""
+        check(_lib.load().bfb_set_small_engine(self.handle, 1 if enabled else 0))
+
+    @property
+    def small_engine_active(self):
+        """True if the next top-down bfs() runs on the single-CTA engine."""
+        return bool(_lib.load().bfb_small_engine_active(self.handle))
+
     def set_timing(self, enabled):
         check(_lib.load().bfb_set_timing(self.handle, 1 if enabled else 0))
 

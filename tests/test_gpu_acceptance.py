@@ -38,12 +38,21 @@ def _spec_graphs():
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("small", [True, False], ids=["single-cta", "level-sync"])
 @pytest.mark.parametrize("name", ["rmat14", "gnp", "path", "star", "components"])
-def test_acceptance1_full_sweep(name):
+def test_acceptance1_full_sweep(name, small):
+    """The whole sweep on both engines: the single-CTA engine these graphs get
+    by default, and the level-synchronous one forced -- except on path(10000),
+    whose up to 10,000 levels per run cost the level-synchronous engine a
+    host round trip and O(CN) launches each (the 300-level path in
+    test_gpu_bfs covers it there)."""
+    if name == "path" and not small:
+        pytest.skip("deep path on the level-synchronous engine: see test_deep_graph_levels_*")
     off, adj = dict(_spec_graphs())[name]
     n = off.size - 1
     dg = DeviceGraph.from_csr(off, adj)
     dg.set_checks(True)
+    dg.set_small_engine(small)
     roots = np.random.default_rng(446).choice(n, 20, replace=False)
     ref = {int(r): ob.bfs_top_down(off, adj, int(r)) for r in roots}
     for cn in CNS:
@@ -51,9 +60,10 @@ def test_acceptance1_full_sweep(name):
         for f in sorted({1, min(2, cn), min(4, cn), cn}):
             for strat in ("butterfly", "all2all"):
                 dg.setup(b, f, strat)
+                assert dg.small_engine_active == small
                 for r in roots:
                     r = int(r)
-                    lv, _, sizes, st, hw = dg.bfs(r)
+                    lv, _, sizes, st, hw = dg.bfs(r, max_levels=n + 1)
                     assert np.array_equal(lv, ref[r]), (name, cn, f, strat, r)
                     assert max(hw) <= f * n or strat == "all2all"
                     if strat == "butterfly":

@@ -96,15 +96,19 @@ def _sweep_graphs():
     yield "components", util.components_graph()
 
 
+@pytest.mark.parametrize("small", [True, False], ids=["single-cta", "level-sync"])
 @pytest.mark.parametrize("cn", [1, 2, 3, 4, 7, 8, 9, 12, 16])
-def test_acceptance_sweep_vs_oracle_engine(cn):
+def test_acceptance_sweep_vs_oracle_engine(cn, small):
     """Acceptance 1,3,4,7,8 at reduced root counts: levels
     equal bfs_top_down, RunStats equal the lockstep oracle engine's for both
-    strategies, buffer high-water within f*|V|, rounds = levels*num_rounds."""
+    strategies, buffer high-water within f*|V|, rounds = levels*num_rounds.
+    Both engines: the single-CTA one these small graphs get by default and
+    the level-synchronous one (forced)."""
     rng = np.random.default_rng(100 + cn)
     for name, (off, adj) in _sweep_graphs():
         n = off.size - 1
         g = _g(off, adj)
+        graphs.device_graph(g).set_small_engine(small)
         p = graphs.partition_1d(g, cn)
         roots = rng.choice(n, 3, replace=False)
         for f in sorted({1, min(2, cn), min(4, cn), cn}):
@@ -115,6 +119,7 @@ def test_acceptance_sweep_vs_oracle_engine(cn):
                     d, st = engine.run(g, p, r, engine.EngineConfig(fanout=f, strategy=strat,
                                                                   parents=True))
                     assert np.array_equal(d.d, ref), (name, cn, f, r, strat)
+                    assert graphs.device_graph(g).small_engine_active == small
                     _, ost = oe.run(off, adj, p.boundaries, r, fanout=f, strategy=strat)
                     assert _same_stats(st, ost), (name, cn, f, r, strat, st, ost)
                     assert max(st.buffer_high_water) <= f * n or strat == "all2all"
@@ -289,8 +294,9 @@ def test_config4_s28_ef8_fanout_sweep():
         assert dg.validate(r) == 0
 
 
+@pytest.mark.parametrize("small", [True, False], ids=["single-cta", "level-sync"])
 @pytest.mark.parametrize("cn", [1, 3])
-def test_deep_graph_levels_past_the_level_bitmaps(cn):
+def test_deep_graph_levels_past_the_level_bitmaps(cn, small):
     """Levels 0..31 are materialised from per-level bitmaps at termination,
     deeper ones written directly (kLevelBits = 32): a 300-vertex path plus a
     cycle and an isolated vertex, from both ends and the middle, all parts,
@@ -298,6 +304,7 @@ def test_deep_graph_levels_past_the_level_bitmaps(cn):
     edges = [(i, i + 1) for i in range(299)] + [(300, 301), (301, 302), (302, 300)]
     off, adj = util.csr_of_undirected(304, edges)
     g = _g(off, adj)
+    graphs.device_graph(g).set_small_engine(small)
     p = graphs.partition_1d(g, cn)
     for direction in ("top-down", "optimizing", "bottom-up"):
         for root in (0, 150, 299, 301, 303):
@@ -309,8 +316,9 @@ def test_deep_graph_levels_past_the_level_bitmaps(cn):
             assert st.per_level_frontier_size == ob.level_sizes(ref)
 
 
+@pytest.mark.parametrize("small", [True, False], ids=["single-cta", "level-sync"])
 @pytest.mark.parametrize("direction", ["top-down", "optimizing"])
-def test_tiny_and_ragged_graphs(direction):
+def test_tiny_and_ragged_graphs(direction, small):
     """Edge cases of the bitmap/word layout: a single vertex, one edge, a
     vertex count that is not a multiple of 32 (star centred on the last
     vertex, padded words), and 32 isolated vertices plus one edge at the end."""
@@ -319,6 +327,7 @@ def test_tiny_and_ragged_graphs(direction):
     for n, edges in cases:
         off, adj = util.csr_of_undirected(n, edges)
         g = _g(off, adj)
+        graphs.device_graph(g).set_small_engine(small)
         for cn in sorted({1, min(2, n), min(3, n)}):
             p = graphs.partition_1d(g, cn)
             for root in sorted({0, n - 1, n // 2}):
