@@ -149,7 +149,8 @@ struct DevGraph {
   const uint32_t* adj_index() const { return adj.p - adj_lo; }
   DevBuf<uint32_t> nonisol;  // bitmap of degree > 0 (bottom-up candidates), built at engine setup
   DevBuf<uint16_t> deg16;    // min(degree, 65535) per vertex (commit degree sums), engine setup
-  DevBuf<uint2> first_nbr;    // two lowest-id neighbours per vertex (bottom-up first probes), engine setup
+  DevBuf<uint32_t> first_nbr; // lowest-id neighbour per vertex, then (second half) the second-lowest
+                              // (parent pass / bottom-up first probes), engine setup
   bool valid = false;
 };
 
@@ -281,6 +282,7 @@ struct bfb_ctx {
   bfb::DevGraph eg;
   bfb::DevBuf<uint32_t> perm, inv;
   bfb::DevBuf<uint32_t> out_level, out_parent;
+  bfb::DevBuf<uint8_t> lv8;  // engine-id levels, one byte each, gathered by the un-permute
   // small graphs: the whole BFS in one single-CTA launch (small_bfs.cu);
   // built at engine setup when the graph qualifies, used for top-down runs
   // while small_mode is on (bfb_set_small_engine)

@@ -78,7 +78,8 @@ struct PartView {
   const int64_t* off;  // CSR offsets (rows of q_v)
   const uint32_t* nonisol;  // degree > 0 bitmap
   const uint16_t* deg16;    // min(degree, 65535)
-  const uint2* first_nbr;    // two lowest-id neighbours (kNone if absent)
+  const uint32_t* nbr0;      // lowest-id neighbour per vertex (kNone if absent)
+  const uint32_t* nbr1;      // second-lowest (split arrays: the parent pass mostly needs nbr0)
   const uint32_t* adj;       // CSR adjacency (the commit's parent pass)
   const uint32_t* inv;       // relabelled engine graph: engine id -> caller's id (parents are
                              // stored in the caller's ids), nullptr = identity
@@ -124,7 +125,8 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.off = G.offsets.p;
   v.nonisol = G.nonisol.p;
   v.deg16 = G.deg16.p;
-  v.first_nbr = G.first_nbr.p;
+  v.nbr0 = G.first_nbr.p;
+  v.nbr1 = G.first_nbr.p + G.first_nbr.n / 2;
   v.adj = G.adj_index();
   v.inv = ctx->relabeled ? ctx->inv.p : nullptr;
   v.rest_degrees = false;
@@ -678,26 +680,26 @@ __global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t*
       // kPassBatch vertices per lane in flight: their table loads, then
       // their first probes, then the rare second probes / row scans
       for (int k0 = 0; k0 < (int)c; k0 += 32 * kPassBatch) {
-        uint32_t u[kPassBatch];
-        uint2 fn[kPassBatch];
+        uint32_t u[kPassBatch], f0[kPassBatch];
         bool hit[kPassBatch];
 #pragma unroll
         for (int b = 0; b < kPassBatch; ++b) {
           const int k = k0 + b * 32 + lane;
           u[b] = k < (int)c ? (uint32_t)(ubase + list[k]) : kNone;
-          fn[b] = u[b] != kNone ? __ldg(v.first_nbr + u[b]) : make_uint2(kNone, kNone);
+          f0[b] = u[b] != kNone ? __ldg(v.nbr0 + u[b]) : kNone;
         }
 #pragma unroll
         for (int b = 0; b < kPassBatch; ++b)
-          hit[b] = fn[b].x != kNone && in_start(v.start, fn[b].x, pol);
+          hit[b] = f0[b] != kNone && in_start(v.start, f0[b], pol);
 #pragma unroll
         for (int b = 0; b < kPassBatch; ++b) {
           if (u[b] == kNone) continue;
           uint32_t p = kNone;
+          uint32_t f1;
           if (hit[b]) {
-            p = fn[b].x;
-          } else if (fn[b].y != kNone && in_start(v.start, fn[b].y, pol)) {
-            p = fn[b].y;
+            p = f0[b];
+          } else if ((f1 = __ldg(v.nbr1 + u[b])) != kNone && in_start(v.start, f1, pol)) {
+            p = f1;
           } else {
             const int64_t e = __ldg(off + u[b] + 1);
             for (int64_t j = __ldg(off + u[b]) + 2; j < e; ++j) {
@@ -1131,17 +1133,20 @@ __global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* _
         // the two lowest-id neighbours (hubs, on Kronecker graphs) decide most
         // candidates -- all of those with degree <= 2 -- from a per-vertex
         // table read coalesced across the warp; only the rest load the row
-        const uint2 f = __ldg(v.first_nbr + u);
+        const uint32_t fx = __ldg(v.nbr0 + u);
         more = __ldg(v.deg16 + u) > 2;
         ++ex;
-        if ((front[f.x >> 5] >> (f.x & 31)) & 1u) {
+        if ((front[fx >> 5] >> (fx & 31)) & 1u) {
           found = true;
-          par = f.x;
-        } else if (f.y != kNone) {
-          ++ex;
-          if ((front[f.y >> 5] >> (f.y & 31)) & 1u) {
-            found = true;
-            par = f.y;
+          par = fx;
+        } else {
+          const uint32_t fy = __ldg(v.nbr1 + u);
+          if (fy != kNone) {
+            ++ex;
+            if ((front[fy >> 5] >> (fy & 31)) & 1u) {
+              found = true;
+              par = fy;
+            }
           }
         }
       }
@@ -1273,12 +1278,48 @@ __device__ __forceinline__ void store_unit_levels(const LevelSlices& L, int64_t 
   }
 }
 
+// Byte form (relabelled engine graph, whose d_local is only ever read back
+// through the un-permute gather): one byte per vertex -- the level 1..31 from
+// the bitmaps, kLv8Keep where d_local holds it (the root's 0, levels >=
+// kLevelBits written directly), kLv8None unreached.  A quarter of the bytes of
+// the uint32 form, written and then gathered.
+constexpr uint32_t kLv8None = 0xFFu, kLv8Keep = 0xFEu;
+__device__ __forceinline__ void store_unit_levels8(const LevelSlices& L, int64_t w0,
+                                                   uint8_t* __restrict__ lv8, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 3, b0 = (lane & 7) * 4;
+#pragma unroll 2
+  for (int q = 0; q < 8; ++q) {
+    const int j = q * 4 + sub;
+    uint32_t sl[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) sl[k] = __shfl_sync(0xffffffffu, L.s[k], j) >> b0;
+    const uint32_t aj = __shfl_sync(0xffffffffu, L.any, j) >> b0;
+    const uint32_t vj = __shfl_sync(0xffffffffu, L.vis, j) >> b0;
+    const int64_t u0 = ((w0 + j) << 5) + b0;
+    if (u0 >= n) continue;
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) bytes |= spread4(sl[k] & 0xFu) << k;
+    const uint32_t f = aj & 0xFu;
+    const uint32_t keep = spread4(vj & ~f & 0xFu) * 0xFFu;  // visited, in no bitmap
+    bytes |= ~(spread4(f) * 0xFFu);                         // 0xFF where in no bitmap
+    bytes &= ~keep | (kLv8Keep * 0x01010101u);              // ... 0xFE where kept
+    if (u0 + 4 <= n) {
+      *reinterpret_cast<uint32_t*>(lv8 + u0) = bytes;
+    } else {
+      for (int t = 0; u0 + t < n; ++t) lv8[u0 + t] = (uint8_t)(bytes >> (8 * t));
+    }
+  }
+}
+
 // Units are taken two at a time so each warp has both units' bitmap loads in
-// flight before the stores.
+// flight before the stores.  lv8 != nullptr: the byte form instead of d_local.
 __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __restrict__ lvbits,
                                                           int64_t pad, int nl,
                                                           const uint32_t* __restrict__ visited,
-                                                          uint32_t* __restrict__ level, int64_t n) {
+                                                          uint32_t* __restrict__ level,
+                                                          uint8_t* __restrict__ lv8, int64_t n) {
   const int lane = threadIdx.x & 31;
   const int64_t nwords = (n + 31) / 32;
   const int64_t nunits = (nwords + 31) / 32;
@@ -1290,23 +1331,32 @@ __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __rest
     load_level_slices(lvbits, pad, nl, visited, unit * 32 + lane, unit * 32 + lane < nwords, A);
     load_level_slices(lvbits, pad, nl, visited, unit2 * 32 + lane,
                       unit2 < nunits && unit2 * 32 + lane < nwords, B);
-    store_unit_levels(A, unit * 32, level, n);
-    if (unit2 < nunits) store_unit_levels(B, unit2 * 32, level, n);
+    if (lv8) {
+      store_unit_levels8(A, unit * 32, lv8, n);
+      if (unit2 < nunits) store_unit_levels8(B, unit2 * 32, lv8, n);
+    } else {
+      store_unit_levels(A, unit * 32, level, n);
+      if (unit2 < nunits) store_unit_levels(B, unit2 * 32, level, n);
+    }
   }
 }
 
 // ------------------------------------------------------------ outputs ----
 // Results in the caller's ids (relabelled engine graph): out[v] = engine
-// result at perm[v], after d_local was materialised in engine ids.  The
-// relabel keeps each degree class in the caller's order, so consecutive v
-// gather from a few ascending streams (isolated vertices: one stream of
-// UNREACHED); each thread keeps kOutBatch vertices' loads in flight (the
-// perm -> gather chain is latency-bound otherwise: 6.6 ms vs 1.x ms at s29).
+// result at perm[v], from the byte form of d_local (lv8; kLv8Keep -> the
+// uint32 d_local).  The relabel keeps each degree class in the caller's
+// order, so consecutive v gather from a few ascending streams (isolated
+// vertices: one stream of UNREACHED); each thread keeps kOutBatch vertices'
+// loads in flight (the perm -> gather chain is latency-bound otherwise: 6.6 ms
+// vs 1.x ms at s29).  Skipping the gathers of isolated vertices (a part
+// lookup per vertex) and capping registers for occupancy measured slower
+// (1.88 -> 2.23 ms at s29): their gathers are cheap sequential streams.
 // Parents are stored in the caller's ids already; an unreached vertex gets
 // none (this also masks a single node's stale entries).  out_level ==
 // nullptr: parents only.
 constexpr int kOutBatch = 8;
 __global__ void __launch_bounds__(256) k_output(const uint32_t* __restrict__ perm,
+                                                const uint8_t* __restrict__ lv8,
                                                 const uint32_t* __restrict__ level,
                                                 const uint32_t* __restrict__ parent,
                                                 uint32_t* __restrict__ out_level,
@@ -1321,7 +1371,10 @@ __global__ void __launch_bounds__(256) k_output(const uint32_t* __restrict__ per
       p[k] = v < n ? __ldg(perm + v) : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < kOutBatch; ++k) l[k] = v0 + k * stride < n ? __ldg(level + p[k]) : kNone;
+    for (int k = 0; k < kOutBatch; ++k) l[k] = v0 + k * stride < n ? __ldg(lv8 + p[k]) : kLv8None;
+#pragma unroll
+    for (int k = 0; k < kOutBatch; ++k)
+      l[k] = l[k] == kLv8None ? kNone : (l[k] == kLv8Keep ? __ldg(level + p[k]) : l[k]);
     if (out_parent) {
 #pragma unroll
       for (int k = 0; k < kOutBatch; ++k) q[k] = l[k] != kNone ? __ldg(parent + p[k]) : kNone;
@@ -1351,7 +1404,8 @@ __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n
 // of degree > 0 and min(degree, 65535) as 16 bits.
 __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                 int64_t n, int64_t row_lo, int64_t row_hi, uint32_t* nonisol,
-                                uint16_t* deg16, uint2* first_nbr, int64_t nwords_pad) {
+                                uint16_t* deg16, uint32_t* nbr0, uint32_t* nbr1,
+                                int64_t nwords_pad) {
   const int lane = threadIdx.x & 31;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords_pad;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -1364,8 +1418,8 @@ __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t*
     // (a rank's partitioned graph holds only its own rows' adjacency; the
     // tables of the other rows are never read)
     const bool mine = u >= row_lo && u < row_hi;
-    first_nbr[u] = make_uint2(mine && d > 0 ? __ldg(adj + o) : kNone,
-                              mine && d > 1 ? __ldg(adj + o + 1) : kNone);
+    nbr0[u] = mine && d > 0 ? __ldg(adj + o) : kNone;
+    nbr1[u] = mine && d > 1 ? __ldg(adj + o + 1) : kNone;
   }
 }
 
@@ -1464,12 +1518,13 @@ unsigned grid_cap(int64_t work, int block, int num_sms, int per_sm = 8) {
 
 // d_local from the level bitmaps at termination (last_level = the deepest
 // level committed); returns kernels launched.
-int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStream_t s) {
+int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStream_t s,
+                              uint8_t* lv8 = nullptr) {
   const int64_t pad = (int64_t)(p.lvbits.n / kLevelBits);
   const int nl = (int)std::min<int64_t>(last_level, kLevelBits - 1);
   k_levels_from_bits<<<resident_grid(k_levels_from_bits, (ctx->g.n + 31) / 32, 256,
                                      ctx->num_sms),
-                       256, 0, s>>>(p.lvbits.p, pad, nl, p.visited.p, p.level.p, ctx->g.n);
+                       256, 0, s>>>(p.lvbits.p, pad, nl, p.visited.p, p.level.p, lv8, ctx->g.n);
   return 1;
 }
 
@@ -1477,10 +1532,11 @@ int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStr
 int launch_output(bfb_ctx* ctx, Part& p, int64_t last_level, const uint32_t* parent, bool levels,
                   cudaStream_t s) {
   int k = 0;
-  if (levels) k += launch_materialise_levels(ctx, p, last_level, s);
+  // (the byte form of d_local: levels=false reuses the run's, for the mask)
+  if (levels) k += launch_materialise_levels(ctx, p, last_level, s, ctx->lv8.p);
   const int64_t n = ctx->g.n;
   k_output<<<grid_cap((n + kOutBatch - 1) / kOutBatch, 256, ctx->num_sms, 8), 256, 0, s>>>(
-      ctx->perm.p, p.level.p, parent, levels ? ctx->out_level.p : nullptr,
+      ctx->perm.p, ctx->lv8.p, p.level.p, parent, levels ? ctx->out_level.p : nullptr,
       parent ? ctx->out_parent.p : nullptr, n);
   return k + 1;
 }
@@ -1686,12 +1742,14 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
   DevGraph& G = EG(ctx);
   BFB_TRY(G.nonisol.alloc(nwords_pad));
   BFB_TRY(G.deg16.alloc((size_t)nwords_pad * 32));
-  BFB_TRY(G.first_nbr.alloc((size_t)nwords_pad * 32));
+  BFB_TRY(G.first_nbr.alloc((size_t)nwords_pad * 64));  // nbr0 | nbr1
   k_vertex_tables<<<grid_cap(nwords_pad * 32, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
       G.offsets.p, G.adj_index(), n, G.row_lo, G.row_hi, G.nonisol.p, G.deg16.p, G.first_nbr.p,
+      G.first_nbr.p + (size_t)nwords_pad * 32,
       nwords_pad);
   if (ctx->relabeled) {
     BFB_TRY(ctx->out_level.alloc(n + 1));
+    BFB_TRY(ctx->lv8.alloc(n + 16));
     if (want_parents) BFB_TRY(ctx->out_parent.alloc(n + 1));
   }
   BFB_CUDA(cudaStreamSynchronize(ctx->stream));
