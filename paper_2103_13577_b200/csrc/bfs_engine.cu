@@ -42,7 +42,11 @@ constexpr int kExpandBlock = 256;
 #ifndef BFB_PASS_SHIFT
 #define BFB_PASS_SHIFT 12
 #endif
-constexpr int kExpandItems = 8;                // edges per lane per subtile
+#ifndef BFB_EXPAND_ITEMS
+#define BFB_EXPAND_ITEMS 8
+#endif
+// edges per lane per subtile (s29 TD, relabelled, 12 roots: 4 250.0, 8 274.5-276.4, 16 274.6)
+constexpr int kExpandItems = BFB_EXPAND_ITEMS;
 constexpr int64_t kSub = 32 * kExpandItems;     // edges per subtile (one warp pass)
 constexpr int kSubPerTile = 8;
 constexpr int64_t kTile = kSub * kSubPerTile;   // edges per tile (tile_vstart granularity)
