@@ -433,13 +433,31 @@ int expand_occupancy(int* occ) {
 }
 
 // ------------------------------------------------------------ phase 2 ----
+// The phase-2 and commit sweeps over whole bitmaps (k_publish, k_merge,
+// k_publish_q, k_merge_mail, k_commit_rest) move 4 words per lane per step
+// (16-byte loads and stores): one word per lane left them latency-bound at
+// ~2 TB/s.  Bitmaps are allocated with kWordPad padding words, zero beyond
+// n, so the last chunk may run past nwords.
+__device__ __forceinline__ uint4 ld4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ void st4(uint32_t* p, uint4 x) { *reinterpret_cast<uint4*>(p) = x; }
+__device__ __forceinline__ uint4 andnot4(uint4 a, uint4 b) {
+  return make_uint4(a.x & ~b.x, a.y & ~b.y, a.z & ~b.z, a.w & ~b.w);
+}
+__device__ __forceinline__ int popc4(uint4 a) {
+  return __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+}
+__device__ __forceinline__ uint32_t word4(uint4 a, int k) {
+  return k == 0 ? a.x : (k == 1 ? a.y : (k == 2 ? a.z : a.w));
+}
+
 __global__ void k_publish(PartView v, int parity) {
   int64_t cnt = 0;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < v.nwords;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t p = v.visited[w] & ~v.start[w];
-    v.pub[w] = p;
-    cnt += __popc(p);
+  const int64_t nq = (v.nwords + 3) >> 2;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 p = andnot4(ld4(v.visited + 4 * q), ld4(v.start + 4 * q));
+    st4(v.pub + 4 * q, p);
+    cnt += popc4(p);
   }
   __shared__ int64_t red[32];
   cnt = block_sum_i64(cnt, red);
@@ -493,12 +511,18 @@ __global__ void k_merge(RoundDesc rd, uint32_t* const* pubs, uint32_t* const* vi
   if (c->pub_count[parity] == 0) return;
   const uint32_t* __restrict__ pub = pubs[src];
   uint32_t* vis = visiteds[rd.pair_dst[p]];
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t s = pub[w];
-    if (s) {
-      uint32_t nb = s & ~vis[w];
-      if (nb) atomicOr(&vis[w], nb);
+  const int64_t nq = (nwords + 3) >> 2;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 s4 = ld4(pub + 4 * q);
+    if (!(s4.x | s4.y | s4.z | s4.w)) continue;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t sw = word4(s4, k);
+      if (sw) {
+        const uint32_t nb = sw & ~vis[4 * q + k];
+        if (nb) atomicOr(&vis[4 * q + k], nb);
+      }
     }
   }
 }
@@ -1051,32 +1075,48 @@ __global__ void __launch_bounds__(256) k_commit_light(PartView v, uint32_t next_
 // lane = bit for coalesced level stores).
 __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_level) {
   const int lane = threadIdx.x & 31;
-  const int64_t span = v.nwords - (v.whi - v.wlo);  // words outside [wlo, whi)
-  const int64_t nunits = (span + 31) / 32;
+  // 4-word chunks of [0, wlo) and [whi, nwords): chunk indices [0, ca) and
+  // [cb, cn), words of the owned range [wlo, whi) masked out
+  const int64_t ca = (v.wlo + 3) >> 2, cb = max(v.whi >> 2, ca), cn = (v.nwords + 3) >> 2;
+  const int64_t nch = ca + (cn > cb ? cn - cb : 0);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t fr = 0, re = 0;
-  for (int64_t unit = gw; unit < nunits; unit += nw) {
-    const int64_t i = unit * 32 + lane;
-    const int64_t w = i < v.wlo ? i : i + (v.whi - v.wlo);
-    const bool in = i < span;
-    const uint32_t a = in ? v.visited[w] : 0u;
-    const uint32_t nb = a & ~(in ? v.start[w] : 0u);
-    if (v.lvbits && in) v.lvbits[w] = nb;
-    unsigned m = __ballot_sync(0xffffffffu, nb != 0);
-    if (!m) continue;
-    while (m && !v.lvbits) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      const uint32_t x = __shfl_sync(0xffffffffu, nb, j);
-      const int64_t wj = __shfl_sync(0xffffffffu, w, j);
-      if ((x >> lane) & 1u) v.level[(wj << 5) + lane] = next_level;
+  for (int64_t base = gw * 32; base < nch; base += nw * 32) {
+    const int64_t i = base + lane;
+    const bool in = i < nch;
+    const int64_t c = i < ca ? i : cb + (i - ca);
+    const int64_t w0 = 4 * c;
+    uint4 a = make_uint4(0, 0, 0, 0), nb4 = a;
+    if (in) {
+      a = ld4(v.visited + w0);
+      nb4 = andnot4(a, ld4(v.start + w0));
     }
-    if (nb) {
-      fr += __popc(nb);
-      v.start[w] = a;
-      if (v.front) v.front[w] = nb;
-      if (v.rest_degrees) re += word_degree_sum16(nb, w, v.deg16, v.off);
+    uint32_t nbk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t w = w0 + k;
+      const bool mine = in && (w < v.wlo || w >= v.whi) && w < v.nwords;
+      nbk[k] = mine ? word4(nb4, k) : 0u;
+      if (v.lvbits && mine) v.lvbits[w] = nbk[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      unsigned m = __ballot_sync(0xffffffffu, nbk[k] != 0);
+      while (m && !v.lvbits) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t x = __shfl_sync(0xffffffffu, nbk[k], j);
+        const int64_t wj = __shfl_sync(0xffffffffu, w0 + k, j);
+        if ((x >> lane) & 1u) v.level[(wj << 5) + lane] = next_level;
+      }
+      if (nbk[k]) {
+        const int64_t w = w0 + k;
+        fr += __popc(nbk[k]);
+        v.start[w] = word4(a, k);
+        if (v.front) v.front[w] = nbk[k];
+        if (v.rest_degrees) re += word_degree_sum16(nbk[k], w, v.deg16, v.off);
+      }
     }
   }
   __shared__ int64_t red[32];
@@ -2687,16 +2727,17 @@ __global__ void __launch_bounds__(256) k_publish_q(PartView v, int parity, uint3
   const int lane = threadIdx.x & 31;
   int64_t cnt = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t nw_round = (v.nwords + 31) & ~(int64_t)31;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw_round; w += stride) {
-    uint32_t p = 0;
-    if (w < v.nwords) {
-      p = v.visited[w] & ~v.start[w];
-      v.pub[w] = p;
+  const int64_t nq = (v.nwords + 3) >> 2;
+  const int64_t nq_round = (nq + 31) & ~(int64_t)31;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nq_round; c += stride) {
+    uint4 p = make_uint4(0, 0, 0, 0);
+    if (c < nq) {
+      p = andnot4(ld4(v.visited + 4 * c), ld4(v.start + 4 * c));
+      st4(v.pub + 4 * c, p);
     }
-    const int c = __popc(p);
-    cnt += c;
-    int incl = c;
+    const int n4 = popc4(p);
+    cnt += n4;
+    int incl = n4;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, incl, d);
@@ -2709,8 +2750,11 @@ __global__ void __launch_bounds__(256) k_publish_q(PartView v, int parity, uint3
                                               (unsigned long long)tot);
     base = __shfl_sync(0xffffffffu, base, 31);
     if (base + tot > qcap) continue;  // dense snapshot: readers use the bitmap
-    int64_t pos = base + incl - c;
-    for (uint32_t x = p; x; x &= x - 1) q[pos++] = (uint32_t)((w << 5) + __ffs(x) - 1);
+    int64_t pos = base + incl - n4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      for (uint32_t x = word4(p, k); x; x &= x - 1)
+        q[pos++] = (uint32_t)(((4 * c + k) << 5) + __ffs(x) - 1);
   }
   __shared__ int64_t red[32];
   cnt = block_sum_i64(cnt, red);
@@ -2743,13 +2787,22 @@ __global__ void k_merge_mail(RoundSrc R, const int64_t* mail, int parity, int64_
   for (int i = 0; i < R.n; ++i)
     if (mail[kMail * R.id[i] + parity] > qcap) live |= 1ull << i;
   if (!live) return;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t acc = 0;
-    for (uint64_t m = live; m; m &= m - 1) acc |= R.pub[__ffsll((long long)m) - 1][w];
-    if (acc) {
-      const uint32_t cur = vis[w];
-      if (acc & ~cur) vis[w] = cur | acc;
+  const int64_t nq = (nwords + 3) >> 2;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nq;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (uint64_t m = live; m; m &= m - 1) {
+      const uint4 x = ld4(R.pub[__ffsll((long long)m) - 1] + 4 * c);
+      acc.x |= x.x;
+      acc.y |= x.y;
+      acc.z |= x.z;
+      acc.w |= x.w;
+    }
+    if (acc.x | acc.y | acc.z | acc.w) {
+      const uint4 cur = ld4(vis + 4 * c);
+      const uint4 nb = andnot4(acc, cur);
+      if (nb.x | nb.y | nb.z | nb.w)
+        st4(vis + 4 * c, make_uint4(cur.x | acc.x, cur.y | acc.y, cur.z | acc.z, cur.w | acc.w));
     }
   }
 }
