@@ -286,6 +286,7 @@ struct bfb_ctx {
   // small graphs: the whole BFS in one single-CTA launch (small_bfs.cu);
   // built at engine setup when the graph qualifies, used for top-down runs
   // while small_mode is on (bfb_set_small_engine)
+  uint32_t hot_limit = 0xFFFFFFFFu;  // phase-1 probes of ids below it cache in L1 (bfs_engine.cu)
   bfb::SmallEngine* small = nullptr;
   int small_mode = 1;
 };

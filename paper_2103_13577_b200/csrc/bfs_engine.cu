@@ -54,6 +54,7 @@ constexpr int kScanItems = 16;                 // commit unit scan: units per th
 constexpr int64_t kScanTile = 256 * kScanItems;
 constexpr int64_t kWordPad = 1024;  // bitmap allocation padding (words)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kHotLimit = 1u << 20;  // see probe_vertex
 // d_local is materialised once at termination from per-level new-vertex
 // bitmaps (one dense 4-byte word per 32 vertices per level, instead of a
 // scattered 4-byte store per discovered vertex); levels from kLevelBits on
@@ -87,6 +88,7 @@ struct PartView {
   const uint32_t* adj;       // CSR adjacency (the commit's parent pass)
   const uint32_t* inv;       // relabelled engine graph: engine id -> caller's id (parents are
                              // stored in the caller's ids), nullptr = identity
+  uint32_t hot_limit;        // phase-1 probes of ids below it cache in L1 (probe_vertex)
   bool rest_degrees;         // k_commit_rest also sums the degrees of its new vertices
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
@@ -134,6 +136,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.adj = G.adj_index();
   v.inv = ctx->relabeled ? ctx->inv.p : nullptr;
   v.rest_degrees = false;
+  v.hot_limit = ctx->hot_limit;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -242,6 +245,23 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t* p) {
 #endif
 }
 
+// Probe of vertex u's visited word.  In the relabelled single-node engine
+// the hubs are the lowest ids: probes of ids below hot_limit (2^20 vertices,
+// a 128 KB slice of the bitmap, sized to stay in L1 next to the expand's
+// other loads) cache in L1 as usual, the rest bypass L1 allocation
+// (ld.global.L1::no_allocate) so the random cold probes do not evict the hub
+// lines.  s29 TD, 12 roots: no split 275.4, split at 2^18 258.6, 2^19 272.5,
+// 2^20 282.5, 2^21 278.4, 2^22 271.7 GTEP/s; hub probes evict_last /
+// cold evict_first variants were slower.  hot_limit = kNone: every probe
+// default-cached (several parts: each part's hubs sit at its own start).
+__device__ __forceinline__ uint32_t probe_vertex(const uint32_t* visited, uint32_t u,
+                                                 uint32_t hot_limit) {
+  if (u < hot_limit) return probe_word(visited + (u >> 5));
+  uint32_t v;
+  asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(visited + (u >> 5)));
+  return v;
+}
+
 // One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
 // with rb the row holding edge r0 and ve the last row that can matter.
 // Returns the row holding edge r0 + kSub (the next subtile's cursor).
@@ -299,7 +319,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
   uint32_t wv[kExpandItems];
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it)
-    wv[it] = ((done >> it) & 1u) ? probe_word(visited + (u[it] >> 5)) : 0xFFFFFFFFu;
+    wv[it] = ((done >> it) & 1u) ? probe_vertex(visited, u[it], v.hot_limit) : 0xFFFFFFFFu;
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
     const uint32_t bit = 1u << (u[it] & 31);
@@ -339,7 +359,7 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
       const int r = k + it * 32 + lane;
-      wv[it] = r < span ? probe_word(visited + (u[it] >> 5)) : 0xFFFFFFFFu;
+      wv[it] = r < span ? probe_vertex(visited, u[it], v.hot_limit) : 0xFFFFFFFFu;
     }
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
@@ -1890,6 +1910,8 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
     D->part_ev.resize(parts + 1);
     for (auto& ev : D->part_ev) BFB_CUDA(cudaEventCreate(&ev));
   }
+  // one node over the relabelled graph: its hubs are the lowest ids (probe_vertex)
+  ctx->hot_limit = ctx->relabeled && parts == 1 ? kHotLimit : kNone;
   ctx->engine_ready = true;
   return BFB_OK;
 }
@@ -2363,6 +2385,8 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   ctx->num_parts = parts;
   ctx->fanout = fanout;
   ctx->bounds.assign(bounds, bounds + parts + 1);
+  // hubs sit at every part's start of the global relabel: probes stay default-cached
+  ctx->hot_limit = parts == 1 ? ctx->hot_limit : kNone;
   EngineTables* D = ctx->tables;
   D->rank = rank;
   Part& p = ctx->parts[0];
