@@ -54,7 +54,10 @@ constexpr int kScanItems = 16;                 // commit unit scan: units per th
 constexpr int64_t kScanTile = 256 * kScanItems;
 constexpr int64_t kWordPad = 1024;  // bitmap allocation padding (words)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr uint32_t kHotLimit = 1u << 20;  // see probe_vertex
+#ifndef BFB_HOT_LIMIT
+#define BFB_HOT_LIMIT (1u << 20)
+#endif
+constexpr uint32_t kHotLimit = BFB_HOT_LIMIT;  // see probe_vertex
 // d_local is materialised once at termination from per-level new-vertex
 // bitmaps (one dense 4-byte word per 32 vertices per level, instead of a
 // scattered 4-byte store per discovered vertex); levels from kLevelBits on
@@ -252,7 +255,9 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t* p) {
 // (ld.global.L1::no_allocate) so the random cold probes do not evict the hub
 // lines.  s29 TD, 12 roots: no split 275.4, split at 2^18 258.6, 2^19 272.5,
 // 2^20 282.5, 2^21 278.4, 2^22 271.7 GTEP/s; hub probes evict_last /
-// cold evict_first variants were slower.  hot_limit = kNone: every probe
+// cold evict_first variants were slower; 1.25 x 2^20, hub probes evict_last
+// and the q_local row loads without L1 allocation are within the +-3%
+// run-to-run drift of one gpurun call (16 roots, interleaved A/B).  hot_limit = kNone: every probe
 // default-cached (several parts: each part's hubs sit at its own start).
 __device__ __forceinline__ uint32_t probe_vertex(const uint32_t* visited, uint32_t u,
                                                  uint32_t hot_limit) {
