@@ -43,12 +43,16 @@ constexpr int kExpandBlock = 256;
 #define BFB_PASS_SHIFT 12
 #endif
 #ifndef BFB_EXPAND_ITEMS
-#define BFB_EXPAND_ITEMS 8
+#define BFB_EXPAND_ITEMS 12
 #endif
-// edges per lane per subtile (s29 TD, relabelled, 12 roots: 4 250.0, 8 274.5-276.4, 16 274.6)
+// edges per lane per subtile (s29 TD, 16 roots, with the L1/L2 probe policies:
+// 10 294.7, 12 297.8, 14 294.4, 16 288.9 GTEP/s; before them 8 was best)
 constexpr int kExpandItems = BFB_EXPAND_ITEMS;
 constexpr int64_t kSub = 32 * kExpandItems;     // edges per subtile (one warp pass)
-constexpr int kSubPerTile = 8;
+#ifndef BFB_SUB_PER_TILE
+#define BFB_SUB_PER_TILE 8
+#endif
+constexpr int kSubPerTile = BFB_SUB_PER_TILE;
 constexpr int64_t kTile = kSub * kSubPerTile;   // edges per tile (tile_vstart granularity)
 constexpr int kScanItems = 16;                 // commit unit scan: units per thread
 constexpr int64_t kScanTile = 256 * kScanItems;
@@ -253,7 +257,8 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t* p) {
 // a 128 KB slice of the bitmap, sized to stay in L1 next to the expand's
 // other loads) cache in L1 as usual, the rest bypass L1 allocation
 // (ld.global.L1::no_allocate) so the random cold probes do not evict the hub
-// lines.  s29 TD, 12 roots: no split 275.4, split at 2^18 258.6, 2^19 272.5,
+// lines, with an L2 evict_last hint so they keep the bitmap resident in L2
+// against the streamed adjacency (+1.9%, 16 roots).  s29 TD, 12 roots: no split 275.4, split at 2^18 258.6, 2^19 272.5,
 // 2^20 282.5, 2^21 278.4, 2^22 271.7 GTEP/s; hub probes evict_last /
 // cold evict_first variants were slower; 1.25 x 2^20, hub probes evict_last
 // and the q_local row loads without L1 allocation are within the +-3%
@@ -263,7 +268,10 @@ __device__ __forceinline__ uint32_t probe_vertex(const uint32_t* visited, uint32
                                                  uint32_t hot_limit) {
   if (u < hot_limit) return probe_word(visited + (u >> 5));
   uint32_t v;
-  asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(visited + (u >> 5)));
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v) : "l"(visited + (u >> 5)), "l"(pol));
   return v;
 }
 
