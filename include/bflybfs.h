@@ -69,6 +69,8 @@ typedef struct bfb_run_stats {
                                         (level + 1) x the next frontier's degree sum
                                         that fed Beamer's rule -- equal on every node
                                         (rank mode) and to the one-context run */
+  int64_t sparse_levels;             /* levels committed from the claim queue
+                                        (bfb_set_sparse_levels)                       */
 } bfb_run_stats;
 
 /* Outcome of bfb_parse_text (graphs.py:96-202 ParseError carries the line). */
@@ -131,6 +133,11 @@ int bfb_set_checks(bfb_ctx* ctx, int flags);
  * enabled = 1 (default) uses it whenever the engine setup built its tables;
  * 0 forces the level-synchronous engine.  Applies from the next bfb_bfs. */
 int bfb_set_small_engine(bfb_ctx* ctx, int enabled);
+/* Sparse levels (one node, top-down): a level whose frontier has few edges
+ * (at most max(|V|/256, 2^16), capped at 2^23) queues its phase-1 claims and
+ * is committed from that queue instead of by sweeps over the whole visited
+ * bitmap.  enabled = 1 (default) / 0.  Results are identical either way. */
+int bfb_set_sparse_levels(bfb_ctx* ctx, int enabled);
 /* 1 if the next top-down bfb_bfs runs on the single-CTA engine. */
 int bfb_small_engine_active(bfb_ctx* ctx);
 /* Phase-1 direction (paper contribution 3; SPEC.md:172 keeps

@@ -49,6 +49,7 @@ class RunStatsC(ctypes.Structure):
         ("bottom_up_levels", c_int64),
         ("expand_max_part_ms", c_double),
         ("switch_checksum", c_int64),
+        ("sparse_levels", c_int64),
     ]
 
 
@@ -84,6 +85,7 @@ _SIGNATURES = {
     "bfb_set_checks": (c_int, [c_void_p, c_int]),
     "bfb_set_small_engine": (c_int, [c_void_p, c_int]),
     "bfb_small_engine_active": (c_int, [c_void_p]),
+    "bfb_set_sparse_levels": (c_int, [c_void_p, c_int]),
     "bfb_buffer_bound": (c_int64, [c_int64, c_int]),
     "bfb_create": (c_int, [POINTER(c_void_p), c_int]),
     "bfb_destroy": (None, [c_void_p]),

@@ -167,6 +167,8 @@ struct PartCounters {
   int64_t ex_next;      // top-down phase 1: next tile to hand out (dense levels)
   int64_t rest_edges;   // degree sum of the new vertices outside the owned range
                         // (rank mode, direction-optimizing: the global switch)
+  unsigned long long sq_claims;  // sparse level: claims appended to the claim queue
+  unsigned long long sq_packed;  // sparse commit: (count << 40) + edges, block-aggregated
 };
 
 // Device-resident run statistics (RunStats).
@@ -195,6 +197,7 @@ struct Part {
   DevBuf<uint32_t> pub_q;          // queue-form snapshots, 2 x nwords entries (by parity)
   DevBuf<uint32_t> front;          // level-L frontier bitmap (bottom-up phase 1)
   DevBuf<uint32_t> lvbits;         // per level 1..kLevelBits-1: that level's new-vertex bitmap
+  DevBuf<uint32_t> sparse_q;       // sparse levels: phase-1 claims (single node, top-down)
   DevBuf<uint32_t> q_v;            // q_local vertex ids, ascending
   DevBuf<int64_t> q_pre;           // exclusive degree prefix over q_local
   DevBuf<int64_t> q_base;          // offsets[v] - q_pre (adjacency base per row)
@@ -286,6 +289,8 @@ struct bfb_ctx {
   // small graphs: the whole BFS in one single-CTA launch (small_bfs.cu);
   // built at engine setup when the graph qualifies, used for top-down runs
   // while small_mode is on (bfb_set_small_engine)
+  uint32_t lvbits_valid = 0xFFFFFFFFu;  // levels whose new-vertex bitmap the last run wrote
+  int sparse_mode = 1;                  // sparse levels committed from the claim queue
   uint32_t hot_limit = 0xFFFFFFFFu;  // phase-1 probes of ids below it cache in L1 (bfs_engine.cu)
   bfb::SmallEngine* small = nullptr;
   int small_mode = 1;

@@ -96,6 +96,7 @@ struct PartView {
   const uint32_t* inv;       // relabelled engine graph: engine id -> caller's id (parents are
                              // stored in the caller's ids), nullptr = identity
   uint32_t hot_limit;        // phase-1 probes of ids below it cache in L1 (probe_vertex)
+  uint32_t* sparse_q;        // sparse level: phase 1 appends its claims here (else nullptr)
   bool rest_degrees;         // k_commit_rest also sums the degrees of its new vertices
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
 };
@@ -144,6 +145,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.inv = ctx->relabeled ? ctx->inv.p : nullptr;
   v.rest_degrees = false;
   v.hot_limit = ctx->hot_limit;
+  v.sparse_q = nullptr;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
 }
@@ -275,6 +277,22 @@ __device__ __forceinline__ uint32_t probe_vertex(const uint32_t* visited, uint32
   return v;
 }
 
+// Check-and-set of u's visited bit after a probe saw it clear.
+// Dense levels: a fire-and-forget red.or (the commit finds the new bits as
+// visited & ~start) and every claimant may store a parent.  Sparse levels
+// (v.sparse_q): atomicOr with the old value, the winner appends u to the
+// claim queue the sparse commit works from, and only it stores the parent.
+__device__ __forceinline__ bool claim(const PartView& v, uint32_t* visited, uint32_t u,
+                                      uint32_t bit) {
+  if (!v.sparse_q) {
+    atomicOr(&visited[u >> 5], bit);
+    return true;
+  }
+  if (atomicOr(&visited[u >> 5], bit) & bit) return false;
+  v.sparse_q[atomicAdd(&v.ctr->sq_claims, 1ull)] = u;
+  return true;
+}
+
 // One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
 // with rb the row holding edge r0 and ve the last row that can matter.
 // Returns the row holding edge r0 + kSub (the next subtile's cursor).
@@ -336,8 +354,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
     const uint32_t bit = 1u << (u[it] & 31);
-    if (!(wv[it] & bit)) {
-      atomicOr(&visited[u[it] >> 5], bit);
+    if (!(wv[it] & bit) && claim(v, visited, u[it], bit)) {
       if (kParents) {
         const uint32_t ro = (rows[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
         v.parent[u[it]] = caller_id(v, __ldg(v.q_v + vs + ro));
@@ -377,8 +394,7 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
       const uint32_t bit = 1u << (u[it] & 31);
-      if (!(wv[it] & bit)) {
-        atomicOr(&visited[u[it] >> 5], bit);
+      if (!(wv[it] & bit) && claim(v, visited, u[it], bit)) {
         if (kParents) v.parent[u[it]] = src;
       }
     }
@@ -1019,6 +1035,66 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
   }
 }
 
+// Commit of a sparse level (one node, top-down): the phase-1 claims (one
+// per new vertex, atomicOr winners) replace the count / scan / write sweeps
+// over the whole bitmap.  Per claimed vertex u: d_local written directly
+// (this level's lvbits slice stays unwritten; the materialisation skips it),
+// u's start bit set, and a q_local row.  Rows and their degree prefix come
+// from one block-aggregated 64-bit atomic on (row count << 40) + edge count,
+// so q_pre is ascending in row order without a device-wide scan; tile starts
+// for the tiles whose first edge falls in the row.  k_sparse_finalize turns
+// the packed totals into the next frontier's counters.
+constexpr int kPackShift = 40;
+__global__ void __launch_bounds__(256) k_sparse_commit(PartView v, const int64_t* __restrict__ off,
+                                                       uint32_t next_level) {
+  __shared__ int64_t wsum[33];
+  __shared__ unsigned long long base;
+  const int64_t nq = (int64_t)v.ctr->sq_claims;
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nq; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;
+    const bool ok = i < nq;
+    uint32_t u = 0;
+    int64_t o = 0, d = 0;
+    if (ok) {
+      u = v.sparse_q[i];
+      o = __ldg(off + u);
+      d = __ldg(off + u + 1) - o;
+      v.level[u] = next_level;
+      atomicOr(&v.start[u >> 5], 1u << (u & 31));
+    }
+    int64_t tot_d;
+    const int64_t ed = block_exclusive_i64(d, wsum, &tot_d);
+    int64_t tot_c;
+    const int64_t ec = block_exclusive_i64(ok ? 1 : 0, wsum, &tot_c);
+    if (threadIdx.x == 0)
+      base = atomicAdd(&v.ctr->sq_packed,
+                       ((unsigned long long)tot_c << kPackShift) + (unsigned long long)tot_d);
+    __syncthreads();
+    const unsigned long long bb = base;
+    __syncthreads();
+    if (ok) {
+      const int64_t row = (int64_t)(bb >> kPackShift) + ec;
+      const int64_t e = (int64_t)(bb & ((1ull << kPackShift) - 1)) + ed;
+      v.q_v[row] = u;
+      v.q_pre[row] = e;
+      v.q_base[row] = o - e;
+      for (int64_t t = (e + kTile - 1) / kTile; t < (e + d + kTile - 1) / kTile; ++t)
+        v.tile_vstart[t] = (uint32_t)row;
+    }
+  }
+}
+
+__global__ void k_sparse_finalize(PartCounters* ctr, RunCounters* run) {
+  const unsigned long long pk = ctr->sq_packed;
+  const int64_t cnt = (int64_t)(pk >> kPackShift), edges = (int64_t)(pk & ((1ull << kPackShift) - 1));
+  ctr->q_count = cnt;
+  ctr->q_edges = edges;
+  ctr->frontier = cnt;
+  ctr->sq_claims = 0;
+  ctr->sq_packed = 0;
+  run->traversed_edges += edges;
+}
+
 // Queue-less commit of a bottom-up level in one pass (the next phase 1 is
 // bottom-up again, which reads only bitmaps): per 32-word unit, levels of the
 // new vertices (lane = bit, coalesced), start := visited, the frontier
@@ -1275,7 +1351,8 @@ struct LevelSlices {
 };
 
 __device__ __forceinline__ void load_level_slices(const uint32_t* __restrict__ lvbits, int64_t pad,
-                                                  int nl, const uint32_t* __restrict__ visited,
+                                                  int nl, uint32_t valid,
+                                                  const uint32_t* __restrict__ visited,
                                                   int64_t wk, bool in, LevelSlices& L) {
 #pragma unroll
   for (int k = 0; k < 5; ++k) L.s[k] = 0u;
@@ -1290,7 +1367,7 @@ __device__ __forceinline__ void load_level_slices(const uint32_t* __restrict__ l
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int l = g0 + j;
-        x[j] = (l < kLevelBits && l <= nl) ? __ldg(lvbits + l * pad + wk) : 0u;
+        x[j] = (l < kLevelBits && l <= nl && ((valid >> l) & 1u)) ? __ldg(lvbits + l * pad + wk) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -1393,7 +1470,7 @@ __device__ __forceinline__ void store_unit_levels8(const LevelSlices& L, int64_t
 // Units are taken two at a time so each warp has both units' bitmap loads in
 // flight before the stores.  lv8 != nullptr: the byte form instead of d_local.
 __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __restrict__ lvbits,
-                                                          int64_t pad, int nl,
+                                                          int64_t pad, int nl, uint32_t valid,
                                                           const uint32_t* __restrict__ visited,
                                                           uint32_t* __restrict__ level,
                                                           uint8_t* __restrict__ lv8, int64_t n) {
@@ -1405,8 +1482,9 @@ __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __rest
        unit += 2 * nw) {
     const int64_t unit2 = unit + nw;
     LevelSlices A, B;
-    load_level_slices(lvbits, pad, nl, visited, unit * 32 + lane, unit * 32 + lane < nwords, A);
-    load_level_slices(lvbits, pad, nl, visited, unit2 * 32 + lane,
+    load_level_slices(lvbits, pad, nl, valid, visited, unit * 32 + lane, unit * 32 + lane < nwords,
+                      A);
+    load_level_slices(lvbits, pad, nl, valid, visited, unit2 * 32 + lane,
                       unit2 < nunits && unit2 * 32 + lane < nwords, B);
     if (lv8) {
       store_unit_levels8(A, unit * 32, lv8, n);
@@ -1601,7 +1679,8 @@ int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStr
   const int nl = (int)std::min<int64_t>(last_level, kLevelBits - 1);
   k_levels_from_bits<<<resident_grid(k_levels_from_bits, (ctx->g.n + 31) / 32, 256,
                                      ctx->num_sms),
-                       256, 0, s>>>(p.lvbits.p, pad, nl, p.visited.p, p.level.p, lv8, ctx->g.n);
+                       256, 0, s>>>(p.lvbits.p, pad, nl, ctx->lvbits_valid, p.visited.p, p.level.p,
+                                    lv8, ctx->g.n);
   return 1;
 }
 
@@ -1848,6 +1927,11 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
     BFB_TRY(p.level.alloc(n + 1));
     if (want_parents) BFB_TRY(p.parent.alloc(n + 1));
     if (parts > 1) BFB_TRY(p.pub.alloc(nwords_pad));
+    if (parts == 1) {
+      // sparse levels' claim queue: frontiers of at most this many edges
+      const int64_t cap = std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(n >> 8, 65536), 1 << 23), n);
+      BFB_TRY(p.sparse_q.alloc(cap));
+    }
     BFB_TRY(p.q_v.alloc(owned + 1));
     BFB_TRY(p.q_pre.alloc(owned + 1));
     BFB_TRY(p.q_base.alloc(owned + 1));
@@ -2043,7 +2127,17 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   int64_t reached = 1;
   int64_t switch_chk = 0;
   const unsigned small_grid = grid_cap(nwords, 256, sms, 4);
+  // sparse levels (one node, top-down): the frontier's edge count bounds the
+  // claims; below the threshold phase 1 queues its claims and the commit works
+  // from the queue (k_sparse_commit) instead of sweeping the bitmaps
+  const bool sparse_ok = ctx->sparse_mode && P == 1 && ctx->direction == 0 &&
+                         ctx->parts[0].sparse_q.p != nullptr;
+  const int64_t sparse_cap = (int64_t)ctx->parts[0].sparse_q.n;
+  int64_t cur_edges = ctx->g.max_degree;  // the root's degree, bounded
+  int64_t sparse_levels = 0;
+  ctx->lvbits_valid = 0xFFFFFFFFu;
   while (true) {
+    const bool sparse = sparse_ok && cur_edges <= sparse_cap;
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
     // Parents of a top-down level with a large frontier come from the
     // commit's parent pass instead of phase-1 stores (k_commit_count): each
@@ -2054,12 +2148,13 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     const bool parent_pass = ctx->want_parents && !bottom_up &&
                              prev_frontier >= std::max<int64_t>(1, n >> 12) &&
                              reached >= (n >> BFB_PASS_SHIFT);
-    const bool expand_parents = ctx->want_parents && !parent_pass;
+    const bool expand_parents = ctx->want_parents && (!parent_pass || sparse);
     // Phase 1
     const bool part_timing = ctx->timing && P > 1;
     for (int g = 0; g < P; ++g) {
       if (part_timing) BFB_CUDA(cudaEventRecord(D->part_ev[g], s));
       PartView v = view_of(ctx, ctx->parts[g]);
+      if (sparse) v.sparse_q = ctx->parts[g].sparse_q.p;
       if (bottom_up) {
         const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
         unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
@@ -2117,7 +2212,17 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     // Bottom-up level: one queue-less pass; the queue is rebuilt from the
     // frontier bitmap only on the switch back to top-down.
     const bool light = ctx->direction != 0 && bottom_up;
-    for (int g = 0; g < P; ++g) {
+    if (sparse) {
+      Part& p = ctx->parts[0];
+      PartView v = view_of(ctx, p);
+      v.sparse_q = p.sparse_q.p;
+      k_sparse_commit<<<grid_cap(sparse_cap, 256, sms, 8), 256, 0, s>>>(v, off, next_level);
+      k_sparse_finalize<<<1, 1, 0, s>>>(p.ctr.p, ctx->run.p);
+      launches += 2;
+      if (next_level < (uint32_t)kLevelBits) ctx->lvbits_valid &= ~(1u << next_level);
+      ++sparse_levels;
+    }
+    for (int g = 0; g < P && !sparse; ++g) {
       Part& p = ctx->parts[g];
       PartView v = commit_view_of(ctx, p, next_level);
       if (p.whi > p.wlo) {
@@ -2158,7 +2263,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       else if (bottom_up && (double)frontier < (double)n / ctx->do_beta && frontier < prev_frontier)
         next_bu = false;
     }
-    for (int g = 0; g < P; ++g) {
+    for (int g = 0; g < P && !sparse; ++g) {
       Part& p = ctx->parts[g];
       if (p.whi <= p.wlo) continue;
       if (light) {
@@ -2171,11 +2276,13 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       }
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
-    if (frontier < 0)
-      BFB_CUDA(cudaMemcpyAsync(ctx->pinned, &ctx->parts[0].ctr.p->frontier, sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, s));
+    // node 0's counters: q_count, q_edges (the next frontier's edges, for
+    // the sparse decision), frontier
+    BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 5, ctx->parts[0].ctr.p, 3 * sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaStreamSynchronize(s));
     BFB_CUDA(cudaGetLastError());
+    cur_edges = P == 1 ? ctx->pinned[6] : INT64_MAX;
     if (ctx->timing) {
       float a = 0, b = 0, c = 0;
       BFB_CUDA(cudaEventElapsedTime(&a, D->ev[2], D->ev[3]));
@@ -2192,7 +2299,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
       }
       t_expand_max += part_timing ? mx : a;
     }
-    frontier = ctx->pinned[0];
+    frontier = ctx->pinned[7];
     if (frontier == 0) break;
     bottom_up = next_bu;
     prev_frontier = frontier;
@@ -2270,6 +2377,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     st->bottom_up_levels = bu_levels;
     st->expand_max_part_ms = t_expand_max;
     st->switch_checksum = switch_chk;
+    st->sparse_levels = sparse_levels;
   }
   if (rc.disagree)
     return fail(BFB_ERR_CAPACITY, "frontier disagreement after phase 2 (" +
@@ -2505,6 +2613,7 @@ int rank_begin(bfb_ctx* ctx, int64_t root) {
   D->levels = 1;
   D->reached = 1;
   ctx->last_sizes.assign(1, 1);
+  ctx->lvbits_valid = 0xFFFFFFFFu;
   D->launches = 1;
   D->remote_messages = D->remote_vertices = D->high_water = D->exchange_bytes = 0;
   ctx->last_root = root;

@@ -227,6 +227,12 @@ int bfb_set_small_engine(bfb_ctx* ctx, int enabled) {
   return BFB_OK;
 }
 
+int bfb_set_sparse_levels(bfb_ctx* ctx, int enabled) {
+  CTX_GUARD(ctx);
+  ctx->sparse_mode = enabled != 0;
+  return BFB_OK;
+}
+
 int bfb_small_engine_active(bfb_ctx* ctx) {
   if (!ctx) return 0;
   std::lock_guard<std::mutex> lock(ctx->mu);

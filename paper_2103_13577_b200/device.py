@@ -262,6 +262,11 @@ class DeviceGraph:
         launch (True, default) or force the level-synchronous engine (False)."""
         check(_lib.load().bfb_set_small_engine(self.handle, 1 if enabled else 0))
 
+    def set_sparse_levels(self, enabled=True):
+        """One node, top-down: commit levels with few frontier edges from the
+        phase-1 claim queue (True, default) or always by bitmap sweeps."""
+        check(_lib.load().bfb_set_sparse_levels(self.handle, 1 if enabled else 0))
+
     @property
     def small_engine_active(self):
         """True if the next top-down bfs() runs on the single-CTA engine."""

@@ -361,3 +361,45 @@ def test_config5_s29_ef8_headline_properties():
             del lv
         assert out["top-down"] == out["optimizing"], int(r)
     dg.set_direction("top-down")
+
+
+@pytest.mark.parametrize("parents", [False, True])
+def test_sparse_levels_identical(golden, parents):
+    """One node, top-down: levels whose frontier has few edges queue their
+    phase-1 claims and are committed from that queue (no sweep over the
+    bitmaps; d_local written directly).  Levels, frontier sizes and traversed
+    edges equal the golden files and the sweep-committed run; parents valid;
+    the device certificate holds."""
+    e = golden["s20_ef8"]
+    g = graphs.kronecker(20, 8, 1)
+    dg = g.device
+    dg.setup(dg.partition_1d(1), 1, "butterfly", parents=parents)
+    for r, want in list(e["bfs"].items())[:3]:
+        r = int(r)
+        out = {}
+        for sparse in (True, False):
+            dg.set_sparse_levels(sparse)
+            lv, pa, sizes, st, _ = dg.bfs(r, parents=parents)
+            assert (st.sparse_levels > 0) == sparse, (r, sparse, st.sparse_levels)
+            assert sha16(lv) == want["levels_sha"] and sizes == want["sizes"], (r, sparse)
+            assert dg.validate(r) == 0
+            if parents:
+                assert not ov.check_parents(g.offsets, g.adjacency, r, lv, pa)
+            out[sparse] = st.traversed_edges
+        assert out[True] == out[False]
+    dg.set_sparse_levels(True)
+
+
+def test_sparse_levels_deep_path():
+    """A 40,000-vertex path (above the single-CTA engine's size) from its
+    middle: every level is sparse, levels past kLevelBits are written directly
+    too; equal to the oracle, parents valid."""
+    off, adj = util.path_graph(40000)
+    g = _g(off, adj)
+    p = graphs.partition_1d(g, 1)
+    for root in (0, 20000, 39999):
+        d, st = engine.run(g, p, root, engine.EngineConfig(parents=True))
+        ref = ob.bfs_top_down(off, adj, root)
+        assert np.array_equal(d.d, ref), root
+        assert not ov.check_parents(off, adj, root, d.d, d.parents)
+        assert st.per_level_frontier_size == ob.level_sizes(ref)
