@@ -133,8 +133,9 @@ int bfb_set_checks(bfb_ctx* ctx, int flags);
  * enabled = 1 (default) uses it whenever the engine setup built its tables;
  * 0 forces the level-synchronous engine.  Applies from the next bfb_bfs. */
 int bfb_set_small_engine(bfb_ctx* ctx, int enabled);
-/* Sparse levels (one node, top-down): a level whose frontier has few edges
- * (at most max(|V|/256, 2^16), capped at 2^23) queues its phase-1 claims and
+/* Sparse levels (one node, top-down phase 1, also inside direction-optimizing
+ * runs): a level whose frontier has few edges (at most max(|V|/64, 2^16),
+ * capped at 2^23) queues its phase-1 claims and
  * is committed from that queue instead of by sweeps over the whole visited
  * bitmap.  enabled = 1 (default) / 0.  Results are identical either way. */
 int bfb_set_sparse_levels(bfb_ctx* ctx, int enabled);

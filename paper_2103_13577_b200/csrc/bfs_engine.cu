@@ -1045,6 +1045,12 @@ __global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t*
 // for the tiles whose first edge falls in the row.  k_sparse_finalize turns
 // the packed totals into the next frontier's counters.
 constexpr int kPackShift = 40;
+#ifndef BFB_SPARSE_SHIFT
+#define BFB_SPARSE_SHIFT 6  // sparse levels: at most n >> this many frontier edges
+#endif
+#ifndef BFB_SPARSE_CAP
+#define BFB_SPARSE_CAP (1 << 23)  // ... and at most this many (the packed row count is 24 bits)
+#endif
 __global__ void __launch_bounds__(256) k_sparse_commit(PartView v, const int64_t* __restrict__ off,
                                                        uint32_t next_level) {
   __shared__ int64_t wsum[33];
@@ -1061,6 +1067,7 @@ __global__ void __launch_bounds__(256) k_sparse_commit(PartView v, const int64_t
       d = __ldg(off + u + 1) - o;
       v.level[u] = next_level;
       atomicOr(&v.start[u >> 5], 1u << (u & 31));
+      if (v.front) atomicOr(&v.front[u >> 5], 1u << (u & 31));  // the next bottom-up level's frontier
     }
     int64_t tot_d;
     const int64_t ed = block_exclusive_i64(d, wsum, &tot_d);
@@ -1929,7 +1936,8 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
     if (parts > 1) BFB_TRY(p.pub.alloc(nwords_pad));
     if (parts == 1) {
       // sparse levels' claim queue: frontiers of at most this many edges
-      const int64_t cap = std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(n >> 8, 65536), 1 << 23), n);
+      const int64_t cap = std::min<int64_t>(
+          std::min<int64_t>(std::max<int64_t>(n >> BFB_SPARSE_SHIFT, 65536), BFB_SPARSE_CAP), n);
       BFB_TRY(p.sparse_q.alloc(cap));
     }
     BFB_TRY(p.q_v.alloc(owned + 1));
@@ -2130,14 +2138,14 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   // sparse levels (one node, top-down): the frontier's edge count bounds the
   // claims; below the threshold phase 1 queues its claims and the commit works
   // from the queue (k_sparse_commit) instead of sweeping the bitmaps
-  const bool sparse_ok = ctx->sparse_mode && P == 1 && ctx->direction == 0 &&
+  const bool sparse_ok = ctx->sparse_mode && P == 1 && ctx->direction != 2 &&
                          ctx->parts[0].sparse_q.p != nullptr;
   const int64_t sparse_cap = (int64_t)ctx->parts[0].sparse_q.n;
   int64_t cur_edges = ctx->g.max_degree;  // the root's degree, bounded
   int64_t sparse_levels = 0;
   ctx->lvbits_valid = 0xFFFFFFFFu;
   while (true) {
-    const bool sparse = sparse_ok && cur_edges <= sparse_cap;
+    const bool sparse = sparse_ok && !bottom_up && cur_edges <= sparse_cap;
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
     // Parents of a top-down level with a large frontier come from the
     // commit's parent pass instead of phase-1 stores (k_commit_count): each
