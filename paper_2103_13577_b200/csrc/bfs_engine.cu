@@ -708,8 +708,13 @@ __device__ __forceinline__ int64_t grab_units(PartCounters* ctr, int lane) {
 #endif
 constexpr int kPassBatch = BFB_PASS_BATCH;
 
+#ifdef BFB_COUNT_MINB
+#define BFB_COUNT_LB __launch_bounds__(256, BFB_COUNT_MINB)
+#else
+#define BFB_COUNT_LB __launch_bounds__(256)
+#endif
 template <bool kParents>
-__global__ void __launch_bounds__(256) k_commit_count(PartView v, const int64_t* __restrict__ off) {
+__global__ void BFB_COUNT_LB k_commit_count(PartView v, const int64_t* __restrict__ off) {
   __shared__ uint16_t s_list[kParents ? 256 / 32 : 1][kParents ? 1024 : 1];
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -930,8 +935,13 @@ __device__ __forceinline__ void write_tile_starts(uint32_t* __restrict__ tile_vs
 // current batch's scan and stores, two batches of gathers in flight per warp
 // at 44 registers; the plain build keeps 38 registers and one more CTA per SM
 // for the sparse levels, which are bound by the per-unit bitmap loads.
+#ifdef BFB_WRITE_MINB
+#define BFB_WRITE_LB __launch_bounds__(256, BFB_WRITE_MINB)
+#else
+#define BFB_WRITE_LB __launch_bounds__(256)
+#endif
 template <bool kWide, bool kPrefetch>
-__global__ void __launch_bounds__(256) k_commit_write(PartView v, const int64_t* __restrict__ off,
+__global__ void BFB_WRITE_LB k_commit_write(PartView v, const int64_t* __restrict__ off,
                                                       uint32_t next_level, int64_t pf_min) {
   if ((v.ctr->q_count >= pf_min) != kPrefetch) return;
   __shared__ uint16_t s_list[256 / 32][1024];  // unit-local vertex index (word * 32 + bit)
@@ -1258,8 +1268,13 @@ __global__ void __launch_bounds__(256) k_commit_rest(PartView v, uint32_t next_l
 // round trip.
 constexpr int kBuBatch = 2;  // measured: 1 -> 607, 2 -> 611, 4 -> 554, 8 -> 455 GTEP/s (s29 DO)
 
+#ifdef BFB_BU_MINB
+#define BFB_BU_LB __launch_bounds__(256, BFB_BU_MINB)
+#else
+#define BFB_BU_LB __launch_bounds__(256)
+#endif
 template <bool kParents>
-__global__ void __launch_bounds__(256) k_bottom_up(PartView v, const uint32_t* __restrict__ adj,
+__global__ void BFB_BU_LB k_bottom_up(PartView v, const uint32_t* __restrict__ adj,
                                                    unsigned long long* examined) {
   const int lane = threadIdx.x & 31;
   const uint32_t* __restrict__ front = v.front;
@@ -1476,7 +1491,12 @@ __device__ __forceinline__ void store_unit_levels8(const LevelSlices& L, int64_t
 
 // Units are taken two at a time so each warp has both units' bitmap loads in
 // flight before the stores.  lv8 != nullptr: the byte form instead of d_local.
-__global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __restrict__ lvbits,
+#ifdef BFB_LEVELS_MINB
+#define BFB_LEVELS_LB __launch_bounds__(256, BFB_LEVELS_MINB)
+#else
+#define BFB_LEVELS_LB __launch_bounds__(256)
+#endif
+__global__ void BFB_LEVELS_LB k_levels_from_bits(const uint32_t* __restrict__ lvbits,
                                                           int64_t pad, int nl, uint32_t valid,
                                                           const uint32_t* __restrict__ visited,
                                                           uint32_t* __restrict__ level,
@@ -1516,8 +1536,19 @@ __global__ void __launch_bounds__(256) k_levels_from_bits(const uint32_t* __rest
 // Parents are stored in the caller's ids already; an unreached vertex gets
 // none (this also masks a single node's stale entries).  out_level ==
 // nullptr: parents only.
-constexpr int kOutBatch = 8;
-__global__ void __launch_bounds__(256) k_output(const uint32_t* __restrict__ perm,
+// vertices per thread in flight x resident blocks per SM (s29, 16 roots,
+// TD / DO GTEP/s): 8 x 4 (62 regs) 298.7 / 995, 16 x 2 269.7 / 731,
+// 12 x 3 292.6 / 927, 2 x 8 300 / 1021, 4 x 6 300 / 1014, 4 x 8 (32 regs,
+// full occupancy) 305 / 1075: the gathers are latency-bound, warps beat
+// per-thread batches
+#ifndef BFB_OUT_BATCH
+#define BFB_OUT_BATCH 4
+#endif
+#ifndef BFB_OUT_MINB
+#define BFB_OUT_MINB 8
+#endif
+constexpr int kOutBatch = BFB_OUT_BATCH;
+__global__ void __launch_bounds__(256, BFB_OUT_MINB) k_output(const uint32_t* __restrict__ perm,
                                                 const uint8_t* __restrict__ lv8,
                                                 const uint32_t* __restrict__ level,
                                                 const uint32_t* __restrict__ parent,
