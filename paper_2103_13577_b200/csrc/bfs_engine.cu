@@ -58,6 +58,8 @@ constexpr int kScanItems = 16;                 // commit unit scan: units per th
 constexpr int64_t kScanTile = 256 * kScanItems;
 constexpr int64_t kWordPad = 1024;  // bitmap allocation padding (words)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+// rank mode: int64 slots per writer in a node's mailbox (see k_signal)
+constexpr int kMail = 5;
 #ifndef BFB_HOT_LIMIT
 #define BFB_HOT_LIMIT (1u << 20)
 #endif
@@ -1071,25 +1073,34 @@ __global__ void __launch_bounds__(256) k_sparse_commit(PartView v, const int64_t
     const bool ok = i < nq;
     uint32_t u = 0;
     int64_t o = 0, d = 0;
+    bool own = false;
     if (ok) {
       u = v.sparse_q[i];
-      o = __ldg(off + u);
-      d = __ldg(off + u + 1) - o;
       v.level[u] = next_level;
       atomicOr(&v.start[u >> 5], 1u << (u & 31));
       if (v.front) atomicOr(&v.front[u >> 5], 1u << (u & 31));  // the next bottom-up level's frontier
+      own = (int64_t)u >= v.lo && (int64_t)u < v.hi;
+      if (own) {
+        o = __ldg(off + u);
+        d = __ldg(off + u + 1) - o;
+      } else if (v.rest_degrees) {
+        // rank mode, direction-optimizing: the next frontier's non-owned edges
+        atomicAdd((unsigned long long*)&v.ctr->rest_edges,
+                  (unsigned long long)(__ldg(off + u + 1) - __ldg(off + u)));
+      }
     }
+    // q_local rows: the owned new vertices only (one node: all of them)
     int64_t tot_d;
     const int64_t ed = block_exclusive_i64(d, wsum, &tot_d);
     int64_t tot_c;
-    const int64_t ec = block_exclusive_i64(ok ? 1 : 0, wsum, &tot_c);
+    const int64_t ec = block_exclusive_i64(own ? 1 : 0, wsum, &tot_c);
     if (threadIdx.x == 0)
       base = atomicAdd(&v.ctr->sq_packed,
                        ((unsigned long long)tot_c << kPackShift) + (unsigned long long)tot_d);
     __syncthreads();
     const unsigned long long bb = base;
     __syncthreads();
-    if (ok) {
+    if (own) {
       const int64_t row = (int64_t)(bb >> kPackShift) + ec;
       const int64_t e = (int64_t)(bb & ((1ull << kPackShift) - 1)) + ed;
       v.q_v[row] = u;
@@ -1106,7 +1117,7 @@ __global__ void k_sparse_finalize(PartCounters* ctr, RunCounters* run) {
   const int64_t cnt = (int64_t)(pk >> kPackShift), edges = (int64_t)(pk & ((1ull << kPackShift) - 1));
   ctr->q_count = cnt;
   ctr->q_edges = edges;
-  ctr->frontier = cnt;
+  ctr->frontier = (int64_t)ctr->sq_claims;  // every new vertex, owned or not
   ctr->sq_claims = 0;
   ctr->sq_packed = 0;
   run->traversed_edges += edges;
@@ -2547,6 +2558,11 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   ctx->bounds.assign(bounds, bounds + parts + 1);
   // hubs sit at every part's start of the global relabel: probes stay default-cached
   ctx->hot_limit = parts == 1 ? ctx->hot_limit : kNone;
+  // host scratch for P nodes (the mailbox copy of rank_bfs)
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  ctx->pinned = nullptr;
+  ++alloc_counter();
+  BFB_CUDA(cudaMallocHost(&ctx->pinned, sizeof(int64_t) * (8 + 8 * (size_t)parts)));
   EngineTables* D = ctx->tables;
   D->rank = rank;
   Part& p = ctx->parts[0];
@@ -2568,8 +2584,8 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   D->peer_pub[0][rank] = p.pub.p;
   D->peer_pub[1][rank] = p.pub_alt.p;
   BFB_TRY(p.pub_q.alloc(2 * (size_t)nwords_pad));
-  BFB_TRY(D->mail.alloc(4 * (size_t)parts));
-  BFB_CUDA(cudaMemset(D->mail.p, 0, 4 * (size_t)parts * sizeof(int64_t)));
+  BFB_TRY(D->mail.alloc(kMail * (size_t)parts));
+  BFB_CUDA(cudaMemset(D->mail.p, 0, kMail * (size_t)parts * sizeof(int64_t)));
   BFB_TRY(D->peer_mail_dev.alloc(parts));
   BFB_TRY(D->err.alloc(1));
   BFB_CUDA(cudaMemset(D->err.p, 0, sizeof(int32_t)));
@@ -2841,10 +2857,11 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 // Mailbox slot of writer w: [kMail*w + parity] = snapshot size of w's last
-// round of that parity, [kMail*w + 2] = w's last published round (seq).  The
+// round of that parity, [kMail*w + 2] = w's last published round (seq),
+// [kMail*w + 3/4] = w's owned share of the committed frontier and its edges
+// (the per-level all-reduce; the edges pick the next level's mode).  The
 // sizes are double-buffered like the snapshots: a writer can run one round
 // ahead of a reader that is still merging, never two.
-constexpr int kMail = 4;
 
 // One thread per peer: write this node's size and seq into its mailbox.
 __global__ void k_signal(int64_t* const* peer_mail, int me, int num_nodes, int64_t seq,
@@ -2883,6 +2900,7 @@ __global__ void k_signal_count(int64_t* const* peer_mail, int me, int num_nodes,
   if (g >= num_nodes || g == me) return;
   int64_t* slot = peer_mail[g] + kMail * me;
   slot[3] = ((volatile const PartCounters*)ctr)->q_count;
+  slot[4] = ((volatile const PartCounters*)ctr)->q_edges;
   st_release_sys(slot + 2, seq);
 }
 
@@ -2949,8 +2967,11 @@ __global__ void __launch_bounds__(256) k_publish_q(PartView v, int parity, uint3
 
 // Queue-form sources of a round: set each listed vertex's bit (several
 // sources and threads may hit one word, so atomically).
+// Sparse levels (sq != nullptr): a vertex this merge sets for the first
+// time is appended to the node's claim queue, which stays the node's whole
+// new-vertex set (the next round's snapshot and the commit's input).
 __global__ void k_merge_queue(RoundSrc R, const int64_t* mail, int parity, int64_t qcap,
-                              uint32_t* __restrict__ vis) {
+                              uint32_t* __restrict__ vis, uint32_t* sq, PartCounters* ctr) {
   for (int i = 0; i < R.n; ++i) {
     const int64_t k = mail[kMail * R.id[i] + parity];
     if (k <= 0 || k > qcap) continue;
@@ -2959,8 +2980,27 @@ __global__ void k_merge_queue(RoundSrc R, const int64_t* mail, int parity, int64
          j += (int64_t)gridDim.x * blockDim.x) {
       const uint32_t u = q[j];
       const uint32_t bit = 1u << (u & 31);
-      if (!(vis[u >> 5] & bit)) atomicOr(&vis[u >> 5], bit);
+      if (vis[u >> 5] & bit) continue;
+      const uint32_t old = atomicOr(&vis[u >> 5], bit);
+      if (sq && !(old & bit)) sq[atomicAdd(&ctr->sq_claims, 1ull)] = u;
     }
+  }
+}
+
+// Sparse-level publish (rank mode): the round-start snapshot is the claim
+// queue itself (phase-1 claims + earlier rounds' merges), copied into this
+// round's queue slot -- O(snapshot) instead of a sweep over the bitmaps.  The
+// snapshot stays below the queue cap (the level's frontier edges bound it),
+// so readers never look at the bitmap form.
+__global__ void k_publish_sparse(const uint32_t* __restrict__ sq, PartCounters* ctr, int parity,
+                                 uint32_t* __restrict__ q) {
+  const int64_t k = (int64_t)ctr->sq_claims;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k;
+       j += (int64_t)gridDim.x * blockDim.x)
+    q[j] = sq[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctr->pub_count[parity] = k;
+    ctr->pub_qpos[parity] = k;
   }
 }
 
@@ -3055,7 +3095,17 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
   if (sizes_out && max_levels > 0) sizes_out[0] = 1;
   double t_expand = 0, t_exchange = 0, t_commit = 0;
   int64_t expand_launches = 0;
+  // sparse levels (as engine_bfs), decided on the GLOBAL frontier edge count
+  // (own share + the peers' shares from the count all-reduce), so every
+  // snapshot of the level stays in queue form: phase 1 queues its claims,
+  // each round publishes the claim queue (no sweep), merges append what they
+  // set, and the commit works from the queue (no sweep of the non-owned words)
+  const bool sparse_ok = ctx->sparse_mode && ctx->direction != 2 && p.sparse_q.p != nullptr;
+  const int64_t sparse_cap = std::min<int64_t>((int64_t)p.sparse_q.n, qcap - 1);
+  int64_t global_edges = ctx->g.max_degree;  // the root's degree, bounded
+  int64_t sparse_levels = 0;
   while (true) {
+    const bool sparse = sparse_ok && !bottom_up && global_edges <= sparse_cap;
     PartView v = view_of(ctx, p);
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
     // parent pass as in engine_bfs, decided from global quantities (every
@@ -3072,10 +3122,13 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       else
         k_bottom_up<false><<<bg, 256, 0, s>>>(v, EG(ctx).adj_index(), ex);
       ++bu_levels;
-    } else if (ctx->want_parents && !parent_pass) {
-      launch_expand<true>(ctx->expand_grid, v, EG(ctx).adj_index(), s);
     } else {
-      launch_expand<false>(ctx->expand_grid, v, EG(ctx).adj_index(), s);
+      PartView ev = v;
+      if (sparse) ev.sparse_q = p.sparse_q.p;
+      if (ctx->want_parents && (!parent_pass || sparse))
+        launch_expand<true>(ctx->expand_grid, ev, EG(ctx).adj_index(), s);
+      else
+        launch_expand<false>(ctx->expand_grid, ev, EG(ctx).adj_index(), s);
     }
     ++launches;
     ++expand_launches;
@@ -3089,18 +3142,23 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
         R.pub[i] = D->peer_pub[parity][R.id[i]];
         R.q[i] = D->peer_q[R.id[i]] + parity * qcap;
       }
-      BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_count[parity], 0, sizeof(int64_t), s));
-      BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_qpos[parity], 0, sizeof(int64_t), s));
-      k_publish_q<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(pv, parity,
-                                                                p.pub_q.p + parity * qcap, qcap);
+      if (sparse) {
+        k_publish_sparse<<<grid_cap(sparse_cap, 256, sms, 2), 256, 0, s>>>(
+            p.sparse_q.p, p.ctr.p, parity, p.pub_q.p + parity * qcap);
+      } else {
+        BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_count[parity], 0, sizeof(int64_t), s));
+        BFB_CUDA(cudaMemsetAsync(&p.ctr.p->pub_qpos[parity], 0, sizeof(int64_t), s));
+        k_publish_q<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(pv, parity,
+                                                                  p.pub_q.p + parity * qcap, qcap);
+      }
       k_signal<<<1, 64, 0, s>>>(D->peer_mail_dev.p, me, P, seq, p.ctr.p, parity);
       k_wait<<<1, 64, 0, s>>>(D->mail.p, me, P, seq, D->err.p, timeout_ns);
       k_account_mail<<<1, 32, 0, s>>>(R, D->mail.p, parity, ctx->run.p, ctx->high_water.p,
                                       bytes_per_transfer, qcap);
       launches += 4;
       if (R.n) {
-        k_merge_queue<<<grid_cap(qcap, 256, sms, 2), 256, 0, s>>>(R, D->mail.p, parity, qcap,
-                                                                   p.visited.p);
+        k_merge_queue<<<grid_cap(qcap, 256, sms, 2), 256, 0, s>>>(
+            R, D->mail.p, parity, qcap, p.visited.p, sparse ? p.sparse_q.p : nullptr, p.ctr.p);
         k_merge_mail<<<grid_cap(nwords, 256, sms, 4), 256, 0, s>>>(R, D->mail.p, parity, qcap,
                                                                   p.visited.p, nwords);
         launches += 2;
@@ -3115,15 +3173,26 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     ++launches;
     if (ctx->direction) BFB_CUDA(cudaMemsetAsync(p.front.p, 0, nwords * sizeof(uint32_t), s));
     const bool light = ctx->direction != 0 && bottom_up;
-    if (p.whi > p.wlo) {
-      if (light)
-        launches += launch_commit_light_count(cv, off, next_level, ctx->run.p, sms, s);
-      else
-        launches += launch_commit_count(cv, off, ctx->run.p, sms, s, parent_pass);
-    }
-    if (nwords - (p.whi - p.wlo) > 0) {
-      k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(cv, next_level);
-      ++launches;
+    if (sparse) {
+      PartView sv = view_of(ctx, p);
+      sv.sparse_q = p.sparse_q.p;
+      sv.rest_degrees = ctx->direction == 1;
+      k_sparse_commit<<<grid_cap(sparse_cap, 256, sms, 8), 256, 0, s>>>(sv, off, next_level);
+      k_sparse_finalize<<<1, 1, 0, s>>>(p.ctr.p, ctx->run.p);
+      launches += 2;
+      if (next_level < (uint32_t)kLevelBits) ctx->lvbits_valid &= ~(1u << next_level);
+      ++sparse_levels;
+    } else {
+      if (p.whi > p.wlo) {
+        if (light)
+          launches += launch_commit_light_count(cv, off, next_level, ctx->run.p, sms, s);
+        else
+          launches += launch_commit_count(cv, off, ctx->run.p, sms, s, parent_pass);
+      }
+      if (nwords - (p.whi - p.wlo) > 0) {
+        k_commit_rest<<<resident_grid(k_commit_rest, nwords, 256, sms), 256, 0, s>>>(cv, next_level);
+        ++launches;
+      }
     }
     bool next_bu = ctx->direction == 2;
     if (ctx->direction == 1) {
@@ -3148,7 +3217,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
       else if (bottom_up && (double)frontier < (double)n / ctx->do_beta && frontier < prev_frontier)
         next_bu = false;
     }
-    if (p.whi > p.wlo) {
+    if (p.whi > p.wlo && !sparse) {
       if (light) {
         if (!next_bu)
           launches += launch_commit_rebuild(cv, off, next_level, ctx->run.p, sms, s);
@@ -3168,8 +3237,14 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned, p.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 4, D->err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (P > 1 && sparse_ok)  // the peers' shares of the next frontier's edges
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 8, D->mail.p, kMail * (size_t)P * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaStreamSynchronize(s));
     BFB_CUDA(cudaGetLastError());
+    global_edges = ctx->pinned[1];
+    for (int g = 0; g < P && sparse_ok; ++g)
+      if (g != me) global_edges += ctx->pinned[8 + kMail * g + 4];
     const int32_t errs = *(int32_t*)(ctx->pinned + 4);
     if (errs & 1) return fail(BFB_ERR_CUDA, "peer barrier timed out (a rank stopped participating)");
     if (errs & 2)
@@ -3214,6 +3289,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     st->commit_ms = t_commit;
     st->expand_launches = expand_launches;
     st->switch_checksum = switch_chk;
+    st->sparse_levels = sparse_levels;
   }
   if (hw > (int64_t)ctx->fanout * n && ctx->strategy == BFB_STRATEGY_BUTTERFLY)
     return fail(BFB_ERR_CAPACITY, "buffer bound violated");

@@ -263,4 +263,5 @@ def aggregate_stats(comm, sizes, st):
         exchange_bytes=int(comm.allreduce(int(st.exchange_bytes))),
         device_ms={"total": float(st.elapsed_ms)},
         kernel_launches=int(st.kernel_launches),
+        sparse_levels=int(getattr(st, "sparse_levels", 0)),
     )

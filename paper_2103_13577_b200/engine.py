@@ -74,6 +74,7 @@ class RunStats:
     kernel_launches: int = 0
     edges_examined: int = 0
     bottom_up_levels: int = 0
+    sparse_levels: int = 0
 
 
 def _check_partition(g, p):
@@ -119,6 +120,7 @@ def stats_of(sizes, st, hw):
         kernel_launches=int(st.kernel_launches),
         edges_examined=int(st.edges_examined),
         bottom_up_levels=int(st.bottom_up_levels),
+        sparse_levels=int(st.sparse_levels),
     )
 
 

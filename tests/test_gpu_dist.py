@@ -52,7 +52,8 @@ def _worker(rank, world, port, cases, out_dir, scale=14):
         np.save(os.path.join(out_dir, f"pa_{rank}_{len(results)}.npy"), d.parents)
         results.append({"sizes": st.per_level_frontier_size, "rm": st.remote_messages,
                         "rv": st.remote_vertices_transferred, "te": st.traversed_edges,
-                        "hw": st.buffer_high_water, "rounds": st.rounds_executed})
+                        "hw": st.buffer_high_water, "rounds": st.rounds_executed,
+                        "sl": st.sparse_levels})
         comm.barrier()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
         json.dump(results, fh)
@@ -210,7 +211,8 @@ def _part_worker(rank, world, port, cases, out_dir, scale):
         np.save(os.path.join(out_dir, f"lv_{rank}_{len(results)}.npy"), d.d)
         np.save(os.path.join(out_dir, f"pa_{rank}_{len(results)}.npy"), d.parents)
         results.append({"sizes": st.per_level_frontier_size, "te": st.traversed_edges,
-                        "rm": st.remote_messages, "rv": st.remote_vertices_transferred})
+                        "rm": st.remote_messages, "rv": st.remote_vertices_transferred,
+                        "sl": st.sparse_levels})
         comm.barrier()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
         json.dump({"info": info, "results": results}, fh)
@@ -259,3 +261,6 @@ def test_partitioned_ranks_s20_golden(golden, world):
                 if direction == "top-down":
                     assert (res["rm"], res["rv"]) == (ost.remote_messages,
                                                       ost.remote_vertices_transferred)
+                # the device-synchronised driver commits the small levels from
+                # the claim queue (no sweeps); the host-sequenced one never does
+                assert (res["sl"] > 0) == cases[i][3], (i, res["sl"])
