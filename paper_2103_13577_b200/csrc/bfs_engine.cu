@@ -284,21 +284,35 @@ __device__ __forceinline__ uint32_t probe_vertex(const uint32_t* visited, uint32
 // visited & ~start) and every claimant may store a parent.  Sparse levels
 // (v.sparse_q): atomicOr with the old value, the winner appends u to the
 // claim queue the sparse commit works from, and only it stores the parent.
+// Append u to a claim queue: one atomic per warp (the lanes appending right
+// now, found by __activemask), so a sparse level with many claims does not
+// serialise on the counter.
+__device__ __forceinline__ void append_claim(uint32_t* sq, unsigned long long* counter,
+                                             uint32_t u) {
+  const unsigned m = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  sq[base + __popc(m & ((1u << lane) - 1u))] = u;
+}
+
+template <bool kSparse>
 __device__ __forceinline__ bool claim(const PartView& v, uint32_t* visited, uint32_t u,
                                       uint32_t bit) {
-  if (!v.sparse_q) {
+  if (!kSparse) {
     atomicOr(&visited[u >> 5], bit);
     return true;
   }
   if (atomicOr(&visited[u >> 5], bit) & bit) return false;
-  v.sparse_q[atomicAdd(&v.ctr->sq_claims, 1ull)] = u;
+  append_claim(v.sparse_q, &v.ctr->sq_claims, u);
   return true;
 }
 
 // One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
 // with rb the row holding edge r0 and ve the last row that can matter.
 // Returns the row holding edge r0 + kSub (the next subtile's cursor).
-template <bool kParents>
+template <bool kParents, bool kSparse>
 __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
                                                    const uint32_t* __restrict__ adj, int64_t r0,
                                                    int span, uint32_t rb, uint32_t ve,
@@ -356,7 +370,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
     const uint32_t bit = 1u << (u[it] & 31);
-    if (!(wv[it] & bit) && claim(v, visited, u[it], bit)) {
+    if (!(wv[it] & bit) && claim<kSparse>(v, visited, u[it], bit)) {
       if (kParents) {
         const uint32_t ro = (rows[it >> 1] >> ((it & 1) * 16)) & 0xFFFFu;
         v.parent[u[it]] = caller_id(v, __ldg(v.q_v + vs + ro));
@@ -374,7 +388,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
 #endif
 constexpr int kRunItems = BFB_RUN_ITEMS;  // s29 TD, tiles from a counter: 8 241.2, 12 241.3, 16 243.5, 20 242.6, 24 241.0 GTEP/s
 
-template <bool kParents>
+template <bool kParents, bool kSparse>
 __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t* __restrict__ adj,
                                                int64_t e0, int span, uint32_t row, uint64_t pol) {
   const int lane = threadIdx.x & 31;
@@ -396,7 +410,7 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
       const uint32_t bit = 1u << (u[it] & 31);
-      if (!(wv[it] & bit) && claim(v, visited, u[it], bit)) {
+      if (!(wv[it] & bit) && claim<kSparse>(v, visited, u[it], bit)) {
         if (kParents) v.parent[u[it]] = src;
       }
     }
@@ -423,7 +437,7 @@ __device__ __forceinline__ uint32_t find_row(const int64_t* __restrict__ q_pre, 
   return lo;
 }
 
-template <bool kParents>
+template <bool kParents, bool kSparse>
 __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
     k_expand_w(PartView v, const uint32_t* __restrict__ adj) {
   const int64_t T = v.ctr->q_edges;
@@ -451,11 +465,11 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       uint32_t cur = v.tile_vstart[t];
       if (cur == ve) {  // the whole tile inside one row
-        expand_row_run<kParents>(v, adj, e0, span, cur, pol);
+        expand_row_run<kParents, kSparse>(v, adj, e0, span, cur, pol);
         continue;
       }
       for (int k = 0; k * kSub < span; ++k)
-        cur = expand_subtile<kParents>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
+        cur = expand_subtile<kParents, kSparse>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
                                        cur, ve, le_mask, pol);
     }
   } else {
@@ -466,20 +480,25 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const uint32_t vs = v.tile_vstart[t];
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       const uint32_t cur = (st % kSubPerTile) ? find_row(v.q_pre, vs, ve, r0) : vs;
-      expand_subtile<kParents>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask, pol);
+      expand_subtile<kParents, kSparse>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask, pol);
     }
   }
 }
 
 // Launch phase 1 (top-down) for one part on stream s.
+// The sparse-level build (claims queued) is a separate instantiation, so the
+// dense levels' kernel carries none of its code (registers).
 template <bool kParents>
 void launch_expand(int grid, const PartView& v, const uint32_t* adj, cudaStream_t s) {
-  k_expand_w<kParents><<<grid, kExpandBlock, 0, s>>>(v, adj);
+  if (v.sparse_q)
+    k_expand_w<kParents, true><<<grid, kExpandBlock, 0, s>>>(v, adj);
+  else
+    k_expand_w<kParents, false><<<grid, kExpandBlock, 0, s>>>(v, adj);
 }
 
 template <bool kParents>
 int expand_occupancy(int* occ) {
-  BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents>, kExpandBlock, 0));
+  BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents, false>, kExpandBlock, 0));
   return BFB_OK;
 }
 
@@ -2982,7 +3001,7 @@ __global__ void k_merge_queue(RoundSrc R, const int64_t* mail, int parity, int64
       const uint32_t bit = 1u << (u & 31);
       if (vis[u >> 5] & bit) continue;
       const uint32_t old = atomicOr(&vis[u >> 5], bit);
-      if (sq && !(old & bit)) sq[atomicAdd(&ctr->sq_claims, 1ull)] = u;
+      if (sq && !(old & bit)) append_claim(sq, &ctr->sq_claims, u);
     }
   }
 }
