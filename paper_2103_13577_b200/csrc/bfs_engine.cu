@@ -94,6 +94,8 @@ struct PartView {
   const uint16_t* deg16;    // min(degree, 65535)
   const uint32_t* nbr0;      // lowest-id neighbour per vertex (kNone if absent)
   const uint32_t* nbr1;      // second-lowest (split arrays: the parent pass mostly needs nbr0)
+  const uint32_t* nbr0c;     // nbr0 in the caller's ids (the parent stored on a hit, loaded beside
+                             // nbr0: no dependent translation before the store)
   const uint32_t* adj;       // CSR adjacency (the commit's parent pass)
   const uint32_t* inv;       // relabelled engine graph: engine id -> caller's id (parents are
                              // stored in the caller's ids), nullptr = identity
@@ -142,7 +144,8 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.nonisol = G.nonisol.p;
   v.deg16 = G.deg16.p;
   v.nbr0 = G.first_nbr.p;
-  v.nbr1 = G.first_nbr.p + G.first_nbr.n / 2;
+  v.nbr1 = G.first_nbr.p + G.first_nbr.n / 3;
+  v.nbr0c = G.first_nbr.p + 2 * (G.first_nbr.n / 3);
   v.adj = G.adj_index();
   v.inv = ctx->relabeled ? ctx->inv.p : nullptr;
   v.rest_degrees = false;
@@ -783,13 +786,14 @@ __global__ void BFB_COUNT_LB k_commit_count(PartView v, const int64_t* __restric
       // kPassBatch vertices per lane in flight: their table loads, then
       // their first probes, then the rare second probes / row scans
       for (int k0 = 0; k0 < (int)c; k0 += 32 * kPassBatch) {
-        uint32_t u[kPassBatch], f0[kPassBatch];
+        uint32_t u[kPassBatch], f0[kPassBatch], c0[kPassBatch];
         bool hit[kPassBatch];
 #pragma unroll
         for (int b = 0; b < kPassBatch; ++b) {
           const int k = k0 + b * 32 + lane;
           u[b] = k < (int)c ? (uint32_t)(ubase + list[k]) : kNone;
           f0[b] = u[b] != kNone ? __ldg(v.nbr0 + u[b]) : kNone;
+          c0[b] = u[b] != kNone ? __ldg(v.nbr0c + u[b]) : kNone;
         }
 #pragma unroll
         for (int b = 0; b < kPassBatch; ++b)
@@ -797,11 +801,13 @@ __global__ void BFB_COUNT_LB k_commit_count(PartView v, const int64_t* __restric
 #pragma unroll
         for (int b = 0; b < kPassBatch; ++b) {
           if (u[b] == kNone) continue;
+          if (hit[b]) {  // the common case: nbr0's caller id was loaded beside nbr0
+            v.parent[u[b]] = c0[b];
+            continue;
+          }
           uint32_t p = kNone;
           uint32_t f1;
-          if (hit[b]) {
-            p = f0[b];
-          } else if ((f1 = __ldg(v.nbr1 + u[b])) != kNone && in_start(v.start, f1, pol)) {
+          if ((f1 = __ldg(v.nbr1 + u[b])) != kNone && in_start(v.start, f1, pol)) {
             p = f1;
           } else {
             const int64_t e = __ldg(off + u[b] + 1);
@@ -1329,7 +1335,7 @@ __global__ void BFB_BU_LB k_bottom_up(PartView v, const uint32_t* __restrict__ a
       const uint32_t vis = __shfl_sync(0xffffffffu, vis_k, jw);
       const uint32_t cand = __shfl_sync(0xffffffffu, cand_k, jw);
       const int64_t u = (w << 5) + lane;
-      bool found = false;
+      bool found = false, first = false;  // first: found at nbr0 (its caller id is tabled)
       uint32_t par = 0;
       const bool is_cand = (cand >> lane) & 1u;
       int64_t b = 0, e = 0;
@@ -1344,6 +1350,7 @@ __global__ void BFB_BU_LB k_bottom_up(PartView v, const uint32_t* __restrict__ a
         if ((front[fx >> 5] >> (fx & 31)) & 1u) {
           found = true;
           par = fx;
+          first = true;
         } else {
           const uint32_t fy = __ldg(v.nbr1 + u);
           if (fy != kNone) {
@@ -1380,7 +1387,7 @@ __global__ void BFB_BU_LB k_bottom_up(PartView v, const uint32_t* __restrict__ a
       }
       const uint32_t nbits = __ballot_sync(0xffffffffu, found);
       if (lane == 0 && nbits) v.visited[w] = vis | nbits;  // this node is the word's only writer
-      if (kParents && found) v.parent[u] = caller_id(v, par);
+      if (kParents && found) v.parent[u] = first ? __ldg(v.nbr0c + u) : caller_id(v, par);
     }
   }
   ex = (unsigned long long)warp_sum_i64((int64_t)ex);
@@ -1628,6 +1635,7 @@ __global__ void k_parents_min(uint32_t* const* parents, int num_nodes, int64_t n
 __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                 int64_t n, int64_t row_lo, int64_t row_hi, uint32_t* nonisol,
                                 uint16_t* deg16, uint32_t* nbr0, uint32_t* nbr1,
+                                uint32_t* nbr0c, const uint32_t* __restrict__ inv,
                                 int64_t nwords_pad) {
   const int lane = threadIdx.x & 31;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords_pad;
@@ -1641,8 +1649,10 @@ __global__ void k_vertex_tables(const int64_t* __restrict__ off, const uint32_t*
     // (a rank's partitioned graph holds only its own rows' adjacency; the
     // tables of the other rows are never read)
     const bool mine = u >= row_lo && u < row_hi;
-    nbr0[u] = mine && d > 0 ? __ldg(adj + o) : kNone;
+    const uint32_t f0 = mine && d > 0 ? __ldg(adj + o) : kNone;
+    nbr0[u] = f0;
     nbr1[u] = mine && d > 1 ? __ldg(adj + o + 1) : kNone;
+    nbr0c[u] = f0 != kNone && inv ? __ldg(inv + f0) : f0;
   }
 }
 
@@ -1966,10 +1976,11 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
   DevGraph& G = EG(ctx);
   BFB_TRY(G.nonisol.alloc(nwords_pad));
   BFB_TRY(G.deg16.alloc((size_t)nwords_pad * 32));
-  BFB_TRY(G.first_nbr.alloc((size_t)nwords_pad * 64));  // nbr0 | nbr1
+  BFB_TRY(G.first_nbr.alloc((size_t)nwords_pad * 96));  // nbr0 | nbr1 | nbr0 in caller ids
   k_vertex_tables<<<grid_cap(nwords_pad * 32, 256, ctx->num_sms, 8), 256, 0, ctx->stream>>>(
       G.offsets.p, G.adj_index(), n, G.row_lo, G.row_hi, G.nonisol.p, G.deg16.p, G.first_nbr.p,
-      G.first_nbr.p + (size_t)nwords_pad * 32,
+      G.first_nbr.p + (size_t)nwords_pad * 32, G.first_nbr.p + (size_t)nwords_pad * 64,
+      ctx->relabeled ? ctx->inv.p : nullptr,
       nwords_pad);
   if (ctx->relabeled) {
     BFB_TRY(ctx->out_level.alloc(n + 1));
