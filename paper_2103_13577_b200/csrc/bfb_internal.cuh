@@ -292,6 +292,7 @@ struct bfb_ctx {
   uint32_t lvbits_valid = 0xFFFFFFFFu;  // levels whose new-vertex bitmap the last run wrote
   int sparse_mode = 1;                  // sparse levels committed from the claim queue
   uint32_t hot_limit = 0xFFFFFFFFu;  // phase-1 probes of ids below it cache in L1 (bfs_engine.cu)
+  bfb::DevBuf<uint32_t> hot_mask;    // several parts: the parts' hub blocks (bfs_engine.cu)
   bfb::SmallEngine* small = nullptr;
   int small_mode = 1;
 };

@@ -100,6 +100,7 @@ struct PartView {
   const uint32_t* inv;       // relabelled engine graph: engine id -> caller's id (parents are
                              // stored in the caller's ids), nullptr = identity
   uint32_t hot_limit;        // phase-1 probes of ids below it cache in L1 (probe_vertex)
+  const uint32_t* hot_mask;  // several parts: 1 bit per 2^16 ids, the parts' hub blocks (or nullptr)
   uint32_t* sparse_q;        // sparse level: phase 1 appends its claims here (else nullptr)
   bool rest_degrees;         // k_commit_rest also sums the degrees of its new vertices
   bool wide;           // max degree >= 2^26: 32-vertex degree sums need 64 bits
@@ -150,6 +151,7 @@ PartView view_of(bfb_ctx* ctx, Part& p) {
   v.inv = ctx->relabeled ? ctx->inv.p : nullptr;
   v.rest_degrees = false;
   v.hot_limit = ctx->hot_limit;
+  v.hot_mask = ctx->hot_mask.n ? ctx->hot_mask.p : nullptr;
   v.sparse_q = nullptr;
   v.wide = ctx->g.max_degree >= ((int64_t)1 << 26);
   return v;
@@ -272,8 +274,10 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t* p) {
 // run-to-run drift of one gpurun call (16 roots, interleaved A/B).  hot_limit = kNone: every probe
 // default-cached (several parts: each part's hubs sit at its own start).
 __device__ __forceinline__ uint32_t probe_vertex(const uint32_t* visited, uint32_t u,
-                                                 uint32_t hot_limit) {
-  if (u < hot_limit) return probe_word(visited + (u >> 5));
+                                                 uint32_t hot_limit, const uint32_t* hot_mask) {
+  const bool hot = hot_mask ? ((__ldg(hot_mask + (u >> 21)) >> ((u >> 16) & 31)) & 1u) != 0
+                            : u < hot_limit;
+  if (hot) return probe_word(visited + (u >> 5));
   uint32_t v;
   uint64_t pol;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -369,7 +373,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
   uint32_t wv[kExpandItems];
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it)
-    wv[it] = ((done >> it) & 1u) ? probe_vertex(visited, u[it], v.hot_limit) : 0xFFFFFFFFu;
+    wv[it] = ((done >> it) & 1u) ? probe_vertex(visited, u[it], v.hot_limit, v.hot_mask) : 0xFFFFFFFFu;
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
     const uint32_t bit = 1u << (u[it] & 31);
@@ -408,7 +412,7 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
       const int r = k + it * 32 + lane;
-      wv[it] = r < span ? probe_vertex(visited, u[it], v.hot_limit) : 0xFFFFFFFFu;
+      wv[it] = r < span ? probe_vertex(visited, u[it], v.hot_limit, v.hot_mask) : 0xFFFFFFFFu;
     }
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
@@ -1920,6 +1924,29 @@ void engine_release(bfb_ctx* ctx) {
   ctx->tables = nullptr;
 }
 
+// Several parts over the relabelled graph: each part's hubs are its first
+// ids, so the hot probes are those of the first kHotLimit / P ids of every
+// part, marked per 2^16-id block (the probe reads one L1-resident word).
+// One part (or no relabel): no mask, the single hot range [0, hot_limit).
+#ifndef BFB_HOT_MASK
+#define BFB_HOT_MASK 1
+#endif
+static int build_hot_mask(bfb_ctx* ctx, const std::vector<int64_t>& b) {
+  ctx->hot_mask.release();
+  const int P = (int)b.size() - 1;
+  if (!BFB_HOT_MASK || !ctx->relabeled || P <= 1) return BFB_OK;
+  const int64_t n = ctx->g.n, nblk = (n + 65535) >> 16;
+  std::vector<uint32_t> m((nblk + 31) / 32 + 1, 0u);
+  for (int g = 0; g < P; ++g) {
+    const int64_t h = std::min<int64_t>(b[g + 1] - b[g], (int64_t)kHotLimit / P);
+    if (h <= 0) continue;
+    for (int64_t k = b[g] >> 16; k <= (b[g] + h - 1) >> 16; ++k) m[k >> 5] |= 1u << (k & 31);
+  }
+  BFB_TRY(ctx->hot_mask.alloc(m.size()));
+  BFB_CUDA(cudaMemcpy(ctx->hot_mask.p, m.data(), m.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  return BFB_OK;
+}
+
 // rb: the partition the engine graph is relabelled within (the engine's own
 // partition, or the global one for a rank's single-node engine)
 static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout,
@@ -2089,6 +2116,7 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
   }
   // one node over the relabelled graph: its hubs are the lowest ids (probe_vertex)
   ctx->hot_limit = ctx->relabeled && parts == 1 ? kHotLimit : kNone;
+  BFB_TRY(build_hot_mask(ctx, rb));
   ctx->engine_ready = true;
   return BFB_OK;
 }
@@ -2588,6 +2616,7 @@ int rank_setup(bfb_ctx* ctx, int parts, const int64_t* bounds, int fanout, int s
   ctx->bounds.assign(bounds, bounds + parts + 1);
   // hubs sit at every part's start of the global relabel: probes stay default-cached
   ctx->hot_limit = parts == 1 ? ctx->hot_limit : kNone;
+  BFB_TRY(build_hot_mask(ctx, ctx->bounds));
   // host scratch for P nodes (the mailbox copy of rank_bfs)
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   ctx->pinned = nullptr;
