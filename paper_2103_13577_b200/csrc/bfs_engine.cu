@@ -604,6 +604,32 @@ __global__ void k_merge(RoundDesc rd, uint32_t* const* pubs, uint32_t* const* vi
   }
 }
 
+// Sparse levels, one context: a round's snapshot of node g is its claim
+// queue's length at the round start; k_merge_sparse pulls the
+// sources' snapshot prefixes and appends what it sets to the receiver's queue
+// (appends land past every snapshot prefix, so a node may be read and
+// written in the same round).
+__global__ void k_snap_sparse(PartCounters** ctrs, int num_nodes, int parity) {
+  for (int g = threadIdx.x; g < num_nodes; g += blockDim.x)
+    ctrs[g]->pub_count[parity] = (int64_t)ctrs[g]->sq_claims;
+}
+
+__global__ void k_merge_sparse(RoundDesc rd, uint32_t* const* sqs, uint32_t* const* visiteds,
+                               PartCounters** ctrs, int parity) {
+  const int p = blockIdx.y;
+  const int src = rd.pair_src[p], dst = rd.pair_dst[p];
+  const int64_t k = ctrs[src]->pub_count[parity];
+  const uint32_t* __restrict__ q = sqs[src];
+  uint32_t* vis = visiteds[dst];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = q[j];
+    const uint32_t bit = 1u << (u & 31);
+    if (vis[u >> 5] & bit) continue;
+    if (!(atomicOr(&vis[u >> 5], bit) & bit)) append_claim(sqs[dst], &ctrs[dst]->sq_claims, u);
+  }
+}
+
 // Checks mode (SPEC.md acceptance 8, frontier agreement): after phase 2 every
 // node's visited bitmap -- levels <= L plus the synchronized frontier -- must
 // equal node 0's; counts the words that differ.
@@ -1871,7 +1897,7 @@ int launch_commit(const PartView& v, const int64_t* off, uint32_t next_level, Ru
 // Device-side tables built at setup (pointer arrays indexed by node, the
 // butterfly rounds as (dst, src) pair lists) and the timing events.
 struct EngineTables {
-  DevBuf<uint32_t*> pubs, visiteds, parents;
+  DevBuf<uint32_t*> pubs, visiteds, parents, sqs;  // sqs: every node's claim queue (sparse levels)
   DevBuf<PartCounters*> ctrs;
   std::vector<DevBuf<int32_t>> round_tables;
   std::vector<RoundDesc> rounds;
@@ -2033,7 +2059,7 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
     BFB_TRY(p.level.alloc(n + 1));
     if (want_parents) BFB_TRY(p.parent.alloc(n + 1));
     if (parts > 1) BFB_TRY(p.pub.alloc(nwords_pad));
-    if (parts == 1) {
+    {
       // sparse levels' claim queue: frontiers of at most this many edges
       const int64_t cap = std::min<int64_t>(
           std::min<int64_t>(std::max<int64_t>(n >> BFB_SPARSE_SHIFT, 65536), BFB_SPARSE_CAP), n);
@@ -2062,10 +2088,16 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
     ctrs[g] = p.ctr.p;
   }
   BFB_TRY(D->pubs.alloc(parts));
+  BFB_TRY(D->sqs.alloc(parts));
   BFB_TRY(D->visiteds.alloc(parts));
   BFB_TRY(D->parents.alloc(parts));
   BFB_TRY(D->ctrs.alloc(parts));
   BFB_CUDA(cudaMemcpy(D->pubs.p, pubs.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
+  {
+    std::vector<uint32_t*> sqs(parts);
+    for (int g = 0; g < parts; ++g) sqs[g] = ctx->parts[g].sparse_q.p;
+    BFB_CUDA(cudaMemcpy(D->sqs.p, sqs.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
+  }
   BFB_CUDA(cudaMemcpy(D->visiteds.p, viss.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
   BFB_CUDA(cudaMemcpy(D->parents.p, pars.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
   BFB_CUDA(cudaMemcpy(D->ctrs.p, ctrs.data(), parts * sizeof(void*), cudaMemcpyHostToDevice));
@@ -2238,7 +2270,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   // sparse levels (one node, top-down): the frontier's edge count bounds the
   // claims; below the threshold phase 1 queues its claims and the commit works
   // from the queue (k_sparse_commit) instead of sweeping the bitmaps
-  const bool sparse_ok = ctx->sparse_mode && P == 1 && ctx->direction != 2 &&
+  const bool sparse_ok = ctx->sparse_mode && ctx->direction != 2 &&
                          ctx->parts[0].sparse_q.p != nullptr;
   const int64_t sparse_cap = (int64_t)ctx->parts[0].sparse_q.n;
   int64_t cur_edges = ctx->g.max_degree;  // the root's degree, bounded
@@ -2290,7 +2322,11 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     for (size_t r = 0; r < D->rounds.size(); ++r) {
       const int parity = (int)(r & 1);
       const RoundDesc& rd = D->rounds[r];
-      for (int g = 0; g < P; ++g) {
+      if (sparse) {  // snapshot = each node's claim queue as it stands
+        k_snap_sparse<<<1, 256, 0, s>>>(D->ctrs.p, P, parity);
+        ++launches;
+      }
+      for (int g = 0; g < P && !sparse; ++g) {
         k_publish<<<small_grid, 256, 0, s>>>(view_of(ctx, ctx->parts[g]), parity);
         ++launches;
       }
@@ -2298,7 +2334,11 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
                                   bytes_per_transfer);
       k_zero_parity<<<1, 256, 0, s>>>(D->ctrs.p, P, parity ^ 1);
       launches += 2;
-      if (rd.npairs) {
+      if (rd.npairs && sparse) {
+        dim3 grid(grid_cap(sparse_cap, 256, sms, 1), rd.npairs);
+        k_merge_sparse<<<grid, 256, 0, s>>>(rd, D->sqs.p, D->visiteds.p, D->ctrs.p, parity);
+        ++launches;
+      } else if (rd.npairs) {
         dim3 grid(grid_cap(nwords, 256, sms, 2), rd.npairs);
         k_merge<<<grid, 256, 0, s>>>(rd, D->pubs.p, D->visiteds.p, D->ctrs.p, parity, nwords);
         ++launches;
@@ -2320,13 +2360,15 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     // Bottom-up level: one queue-less pass; the queue is rebuilt from the
     // frontier bitmap only on the switch back to top-down.
     const bool light = ctx->direction != 0 && bottom_up;
-    if (sparse) {
-      Part& p = ctx->parts[0];
+    for (int g = 0; g < P && sparse; ++g) {
+      Part& p = ctx->parts[g];
       PartView v = view_of(ctx, p);
       v.sparse_q = p.sparse_q.p;
       k_sparse_commit<<<grid_cap(sparse_cap, 256, sms, 8), 256, 0, s>>>(v, off, next_level);
       k_sparse_finalize<<<1, 1, 0, s>>>(p.ctr.p, ctx->run.p);
       launches += 2;
+    }
+    if (sparse) {
       if (next_level < (uint32_t)kLevelBits) ctx->lvbits_valid &= ~(1u << next_level);
       ++sparse_levels;
     }
@@ -2385,12 +2427,16 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     }
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[5], s));
     // node 0's counters: q_count, q_edges (the next frontier's edges, for
-    // the sparse decision), frontier
+    // the sparse decision), frontier; the other nodes' q_edges
     BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 5, ctx->parts[0].ctr.p, 3 * sizeof(int64_t),
                              cudaMemcpyDeviceToHost, s));
+    for (int g = 1; g < P && sparse_ok; ++g)
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 8 + g, &ctx->parts[g].ctr.p->q_edges,
+                               sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     BFB_CUDA(cudaStreamSynchronize(s));
     BFB_CUDA(cudaGetLastError());
-    cur_edges = P == 1 ? ctx->pinned[6] : INT64_MAX;
+    cur_edges = ctx->pinned[6];
+    for (int g = 1; g < P && sparse_ok; ++g) cur_edges += ctx->pinned[8 + g];
     if (ctx->timing) {
       float a = 0, b = 0, c = 0;
       BFB_CUDA(cudaEventElapsedTime(&a, D->ev[2], D->ev[3]));
