@@ -552,6 +552,7 @@ struct RoundDesc {
 
 // One block.  Snapshot sizes live in pub_count[round parity] so a round can
 // zero the other parity for the next one.
+// bytes_per_transfer < 0: queue-form snapshots (sparse levels), 4 B per vertex
 __global__ void k_account(RoundDesc rd, PartCounters** ctrs, RunCounters* run, int64_t* high_water,
                           int parity, int64_t bytes_per_transfer) {
   for (int g = threadIdx.x; g < rd.num_nodes; g += blockDim.x) {
@@ -568,7 +569,7 @@ __global__ void k_account(RoundDesc rd, PartCounters** ctrs, RunCounters* run, i
       atomicAdd((unsigned long long*)&run->remote_messages, (unsigned long long)msgs);
       atomicAdd((unsigned long long*)&run->remote_vertices, (unsigned long long)in);
       atomicAdd((unsigned long long*)&run->exchange_bytes,
-                (unsigned long long)(msgs * bytes_per_transfer));
+                (unsigned long long)(bytes_per_transfer < 0 ? 4 * in : msgs * bytes_per_transfer));
     }
     if (in > high_water[g]) high_water[g] = in;
   }
@@ -2331,7 +2332,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
         ++launches;
       }
       k_account<<<1, 256, 0, s>>>(rd, D->ctrs.p, ctx->run.p, ctx->high_water.p, parity,
-                                  bytes_per_transfer);
+                                  sparse ? -1 : bytes_per_transfer);
       k_zero_parity<<<1, 256, 0, s>>>(D->ctrs.p, P, parity ^ 1);
       launches += 2;
       if (rd.npairs && sparse) {
