@@ -273,10 +273,11 @@ __device__ __forceinline__ uint32_t probe_word(const uint32_t* p) {
 // and the q_local row loads without L1 allocation are within the +-3%
 // run-to-run drift of one gpurun call (16 roots, interleaved A/B).  hot_limit = kNone: every probe
 // default-cached (several parts: each part's hubs sit at its own start).
+template <bool kMask>
 __device__ __forceinline__ uint32_t probe_vertex(const uint32_t* visited, uint32_t u,
                                                  uint32_t hot_limit, const uint32_t* hot_mask) {
-  const bool hot = hot_mask ? ((__ldg(hot_mask + (u >> 21)) >> ((u >> 16) & 31)) & 1u) != 0
-                            : u < hot_limit;
+  const bool hot = kMask ? ((__ldg(hot_mask + (u >> 21)) >> ((u >> 16) & 31)) & 1u) != 0
+                         : u < hot_limit;
   if (hot) return probe_word(visited + (u >> 5));
   uint32_t v;
   uint64_t pol;
@@ -319,7 +320,7 @@ __device__ __forceinline__ bool claim(const PartView& v, uint32_t* visited, uint
 // One subtile: edges [r0, r0 + span) of the frontier, rows vs0.. of q_local
 // with rb the row holding edge r0 and ve the last row that can matter.
 // Returns the row holding edge r0 + kSub (the next subtile's cursor).
-template <bool kParents, bool kSparse>
+template <bool kParents, bool kSparse, bool kMask>
 __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
                                                    const uint32_t* __restrict__ adj, int64_t r0,
                                                    int span, uint32_t rb, uint32_t ve,
@@ -373,7 +374,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
   uint32_t wv[kExpandItems];
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it)
-    wv[it] = ((done >> it) & 1u) ? probe_vertex(visited, u[it], v.hot_limit, v.hot_mask) : 0xFFFFFFFFu;
+    wv[it] = ((done >> it) & 1u) ? probe_vertex<kMask>(visited, u[it], v.hot_limit, v.hot_mask) : 0xFFFFFFFFu;
 #pragma unroll
   for (int it = 0; it < kExpandItems; ++it) {
     const uint32_t bit = 1u << (u[it] & 31);
@@ -395,7 +396,7 @@ __device__ __forceinline__ uint32_t expand_subtile(const PartView& v,
 #endif
 constexpr int kRunItems = BFB_RUN_ITEMS;  // s29 TD, tiles from a counter: 8 241.2, 12 241.3, 16 243.5, 20 242.6, 24 241.0 GTEP/s
 
-template <bool kParents, bool kSparse>
+template <bool kParents, bool kSparse, bool kMask>
 __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t* __restrict__ adj,
                                                int64_t e0, int span, uint32_t row, uint64_t pol) {
   const int lane = threadIdx.x & 31;
@@ -412,7 +413,7 @@ __device__ __forceinline__ void expand_row_run(const PartView& v, const uint32_t
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
       const int r = k + it * 32 + lane;
-      wv[it] = r < span ? probe_vertex(visited, u[it], v.hot_limit, v.hot_mask) : 0xFFFFFFFFu;
+      wv[it] = r < span ? probe_vertex<kMask>(visited, u[it], v.hot_limit, v.hot_mask) : 0xFFFFFFFFu;
     }
 #pragma unroll
     for (int it = 0; it < kRunItems; ++it) {
@@ -444,7 +445,7 @@ __device__ __forceinline__ uint32_t find_row(const int64_t* __restrict__ q_pre, 
   return lo;
 }
 
-template <bool kParents, bool kSparse>
+template <bool kParents, bool kSparse, bool kMask>
 __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
     k_expand_w(PartView v, const uint32_t* __restrict__ adj) {
   const int64_t T = v.ctr->q_edges;
@@ -472,11 +473,11 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       uint32_t cur = v.tile_vstart[t];
       if (cur == ve) {  // the whole tile inside one row
-        expand_row_run<kParents, kSparse>(v, adj, e0, span, cur, pol);
+        expand_row_run<kParents, kSparse, kMask>(v, adj, e0, span, cur, pol);
         continue;
       }
       for (int k = 0; k * kSub < span; ++k)
-        cur = expand_subtile<kParents, kSparse>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
+        cur = expand_subtile<kParents, kSparse, kMask>(v, adj, e0 + k * kSub, min((int)kSub, span - k * (int)kSub),
                                        cur, ve, le_mask, pol);
     }
   } else {
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
       const uint32_t vs = v.tile_vstart[t];
       const uint32_t ve = (t + 1 < ntiles) ? v.tile_vstart[t + 1] : qlast;
       const uint32_t cur = (st % kSubPerTile) ? find_row(v.q_pre, vs, ve, r0) : vs;
-      expand_subtile<kParents, kSparse>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask, pol);
+      expand_subtile<kParents, kSparse, kMask>(v, adj, r0, (int)min(kSub, T - r0), cur, ve, le_mask, pol);
     }
   }
 }
@@ -495,17 +496,26 @@ __global__ void __launch_bounds__(kExpandBlock, BFB_EXPAND_MINB)
 // Launch phase 1 (top-down) for one part on stream s.
 // The sparse-level build (claims queued) is a separate instantiation, so the
 // dense levels' kernel carries none of its code (registers).
+template <bool kParents, bool kMask>
+void launch_expand_m(int grid, const PartView& v, const uint32_t* adj, cudaStream_t s) {
+  if (v.sparse_q)
+    k_expand_w<kParents, true, kMask><<<grid, kExpandBlock, 0, s>>>(v, adj);
+  else
+    k_expand_w<kParents, false, kMask><<<grid, kExpandBlock, 0, s>>>(v, adj);
+}
+// (the hub-block mask of several parts is a separate build too: a runtime
+// choice in the probe cost the one-node kernel 35% more instructions)
 template <bool kParents>
 void launch_expand(int grid, const PartView& v, const uint32_t* adj, cudaStream_t s) {
-  if (v.sparse_q)
-    k_expand_w<kParents, true><<<grid, kExpandBlock, 0, s>>>(v, adj);
+  if (v.hot_mask)
+    launch_expand_m<kParents, true>(grid, v, adj, s);
   else
-    k_expand_w<kParents, false><<<grid, kExpandBlock, 0, s>>>(v, adj);
+    launch_expand_m<kParents, false>(grid, v, adj, s);
 }
 
 template <bool kParents>
 int expand_occupancy(int* occ) {
-  BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents, false>, kExpandBlock, 0));
+  BFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_expand_w<kParents, false, false>, kExpandBlock, 0));
   return BFB_OK;
 }
 
