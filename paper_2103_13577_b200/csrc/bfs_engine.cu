@@ -1189,6 +1189,102 @@ __global__ void k_sparse_finalize(PartCounters* ctr, RunCounters* run) {
   run->traversed_edges += edges;
 }
 
+// Thin levels (one node, top-down): consecutive levels whose frontier has at
+// most kTailEdges edges run inside ONE single-CTA launch -- expand (warp per
+// frontier vertex, lanes over its row, atomicOr winners appended to the
+// claim queue, parents by the winners), then the commit of the claimed
+// vertices (d_local directly, start bit, q_local rows with their degree
+// prefix by a block scan, tile starts) -- with CTA barriers between the
+// steps instead of launches and a host round trip per level.  Long thin tails
+// (the paper's Webbase-2001, "one at each level"; deep paths)
+// cost ~microseconds per level instead of ~20.  The launch stops after
+// kTailMax levels, on an empty frontier, or when the frontier outgrows
+// kTailEdges; the state it leaves (q_local, counters) is the one the
+// level-synchronous passes continue from.
+constexpr int64_t kTailEdges = 1 << 15;
+constexpr int kTailMax = 4096;
+constexpr int kTailThreads = 1024;
+struct TailOut {
+  int64_t levels;  // levels committed (the last may be empty: the BFS ended)
+};
+
+template <bool kParents>
+__global__ void __launch_bounds__(kTailThreads, 1) k_tail(PartView v, const int64_t* __restrict__ off,
+                                                          const uint32_t* __restrict__ adj,
+                                                          uint32_t level0, RunCounters* run,
+                                                          int64_t* sizes, TailOut* out) {
+  __shared__ unsigned long long cnt_s;
+  __shared__ int64_t wsum[33];
+  __shared__ int64_t carry_e, carry_r;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = kTailThreads / 32;
+  uint32_t L = level0;
+  int done = 0;
+  while (done < kTailMax) {
+    const int64_t qn = ((volatile PartCounters*)v.ctr)->q_count;
+    const int64_t qe = ((volatile PartCounters*)v.ctr)->q_edges;
+    if (qn == 0 || qe > kTailEdges) break;
+    if (tid == 0) cnt_s = 0;
+    __syncthreads();
+    // phase 1 over q_local (rows in q_v)
+    for (int64_t k = warp; k < qn; k += nwarps) {
+      const uint32_t x = v.q_v[k];
+      const int64_t e1 = off[x + 1];
+      for (int64_t j = off[x] + lane; j < e1; j += 32) {
+        const uint32_t z = adj[j];
+        const uint32_t bit = 1u << (z & 31);
+        if (__ldcg(v.visited + (z >> 5)) & bit) continue;
+        if (atomicOr(v.visited + (z >> 5), bit) & bit) continue;
+        v.sparse_q[atomicAdd(&cnt_s, 1ull)] = z;
+        if (kParents) v.parent[z] = caller_id(v, x);
+      }
+    }
+    __syncthreads();
+    const int64_t nc = (int64_t)cnt_s;
+    if (tid == 0) carry_e = carry_r = 0;
+    __syncthreads();
+    // commit of the claimed vertices, rows in claim order
+    for (int64_t b0 = 0; b0 < nc; b0 += kTailThreads) {
+      const int64_t i = b0 + tid;
+      uint32_t u = 0;
+      int64_t o = 0, d = 0;
+      if (i < nc) {
+        u = v.sparse_q[i];
+        o = off[u];
+        d = off[u + 1] - o;
+        v.level[u] = L + 1;
+        atomicOr(v.start + (u >> 5), 1u << (u & 31));
+      }
+      int64_t tot;
+      const int64_t ex = block_exclusive_i64(d, wsum, &tot);
+      if (i < nc) {
+        const int64_t e = carry_e + ex;
+        v.q_v[i] = u;
+        v.q_pre[i] = e;
+        v.q_base[i] = o - e;
+        for (int64_t t = (e + kTile - 1) / kTile; t < (e + d + kTile - 1) / kTile; ++t)
+          v.tile_vstart[t] = (uint32_t)i;
+      }
+      __syncthreads();
+      if (tid == 0) carry_e += tot;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      v.ctr->q_count = nc;
+      v.ctr->q_edges = carry_e;
+      v.ctr->frontier = nc;
+      run->traversed_edges += carry_e;
+      sizes[done] = nc;
+    }
+    __threadfence_block();
+    __syncthreads();
+    ++done;
+    ++L;
+    if (nc == 0) break;
+  }
+  if (tid == 0) out->levels = done;
+}
+
 // Queue-less commit of a bottom-up level in one pass (the next phase 1 is
 // bottom-up again, which reads only bitmaps): per 32-word unit, levels of the
 // new vertices (lane = bit, coalesced), start := visited, the frontier
@@ -1913,6 +2009,9 @@ struct EngineTables {
   std::vector<DevBuf<int32_t>> round_tables;
   std::vector<RoundDesc> rounds;
   DevBuf<uint32_t> parents_final;  // assembled output parents when num_parts > 1
+  DevBuf<int64_t> tail_sizes;      // k_tail: frontier sizes of the levels it committed
+  DevBuf<TailOut> tail_out;
+  std::vector<int64_t> tail_host;  // their host copy (sized at setup)
   cudaEvent_t ev[6] = {};
   std::vector<cudaEvent_t> part_ev;  // timing mode, CN > 1: per-node phase-1 bounds
   // multi-process mode (rank >= 0): this context holds node `rank` only
@@ -2142,6 +2241,11 @@ static int engine_setup_rb(bfb_ctx* ctx, int parts, const int64_t* bounds, int f
     D->round_tables.push_back(std::move(tab));
   }
   if (want_parents && parts > 1) BFB_TRY(D->parents_final.alloc(n + 1));
+  if (parts == 1) {  // thin levels run in k_tail
+    BFB_TRY(D->tail_sizes.alloc(kTailMax));
+    BFB_TRY(D->tail_out.alloc(1));
+    D->tail_host.assign(kTailMax + 1, 0);
+  }
   BFB_TRY(ctx->run.alloc(1));
   BFB_TRY(ctx->high_water.alloc(parts));
   BFB_CUDA(cudaMallocHost(&ctx->pinned, sizeof(int64_t) * (8 + 8 * (size_t)parts)));
@@ -2287,7 +2391,54 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
   int64_t cur_edges = ctx->g.max_degree;  // the root's degree, bounded
   int64_t sparse_levels = 0;
   ctx->lvbits_valid = 0xFFFFFFFFu;
+  const bool tail_ok = sparse_ok && P == 1 && ctx->direction == 0 && D->tail_sizes.p != nullptr;
+  bool finished = false;
   while (true) {
+    if (tail_ok && cur_edges <= kTailEdges) {
+      // a run of thin levels in one single-CTA launch (k_tail)
+      Part& tp = ctx->parts[0];
+      PartView tv = view_of(ctx, tp);
+      tv.sparse_q = tp.sparse_q.p;
+      if (ctx->want_parents)
+        k_tail<true><<<1, kTailThreads, 0, s>>>(tv, off, EG(ctx).adj_index(), (uint32_t)level,
+                                                 ctx->run.p, D->tail_sizes.p, D->tail_out.p);
+      else
+        k_tail<false><<<1, kTailThreads, 0, s>>>(tv, off, EG(ctx).adj_index(), (uint32_t)level,
+                                                  ctx->run.p, D->tail_sizes.p, D->tail_out.p);
+      ++launches;
+      ++expand_launches;
+      BFB_CUDA(cudaMemcpyAsync(D->tail_host.data() + kTailMax, D->tail_out.p, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
+      BFB_CUDA(cudaMemcpyAsync(D->tail_host.data(), D->tail_sizes.p, kTailMax * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s));
+      BFB_CUDA(cudaMemcpyAsync(ctx->pinned + 5, tp.ctr.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               s));
+      BFB_CUDA(cudaStreamSynchronize(s));
+      BFB_CUDA(cudaGetLastError());
+      const int64_t nl = D->tail_host[kTailMax];
+      for (int64_t i = 0; i < nl; ++i) {
+        const uint32_t committed = (uint32_t)(level + 1);
+        if (committed < (uint32_t)kLevelBits) ctx->lvbits_valid &= ~(1u << committed);
+        ++sparse_levels;
+        const int64_t f = D->tail_host[i];
+        if (f == 0) {
+          finished = true;
+          break;
+        }
+        prev_frontier = f;
+        if (nsizes < max_levels && sizes_out) sizes_out[nsizes] = f;
+        ctx->last_sizes.push_back(f);
+        ++nsizes;
+        reached += f;
+        ++level;
+      }
+      if (finished) break;
+      cur_edges = ctx->pinned[6];
+      if (level > n) return fail(BFB_ERR_CAPACITY, "level count exceeded |V| (internal error)");
+      if (cur_edges <= kTailEdges && ctx->pinned[5] > 0 && nl < kTailMax)
+        return fail(BFB_ERR_CUDA, "thin-level kernel stopped early (internal error)");
+      continue;
+    }
     const bool sparse = sparse_ok && !bottom_up && cur_edges <= sparse_cap;
     if (ctx->timing) BFB_CUDA(cudaEventRecord(D->ev[2], s));
     // Parents of a top-down level with a large frontier come from the

@@ -403,3 +403,42 @@ def test_sparse_levels_deep_path():
         assert np.array_equal(d.d, ref), root
         assert not ov.check_parents(off, adj, root, d.d, d.parents)
         assert st.per_level_frontier_size == ob.level_sizes(ref)
+
+
+def test_thin_levels_in_one_launch():
+    """Thin levels (frontier edges <= 2^15; one node, top-down) run back to
+    back inside single-CTA launches of up to 4096 levels, continuing from and
+    handing back to the level-synchronous passes: a 200,000-vertex path from
+    one end (49 launches), and a Kronecker s16 graph with a 5,000-vertex tail
+    attached to vertex 0 (dense levels, then the thin tail).  Levels, sizes,
+    traversed edges equal the oracle; parents valid; with the thin-level and
+    sparse paths switched off the results are the same."""
+    off, adj = util.path_graph(200000)
+    g = _g(off, adj)
+    p = graphs.partition_1d(g, 1)
+    d, st = engine.run(g, p, 0, engine.EngineConfig(parents=True))
+    ref = ob.bfs_top_down(off, adj, 0)
+    assert np.array_equal(d.d, ref) and st.levels == 200000
+    assert st.sparse_levels >= 199999
+    assert not ov.check_parents(off, adj, 0, d.d, d.parents)
+    # Kronecker core + a tail
+    koff, kadj = util.rmat_graph(16)
+    n0 = koff.size - 1
+    src = np.repeat(np.arange(n0, dtype=np.int64), np.diff(koff))
+    pairs = np.stack([src, kadj.astype(np.int64)], 1)
+    pairs = pairs[pairs[:, 0] < pairs[:, 1]]
+    tail = [(0, n0)] + [(n0 + i, n0 + i + 1) for i in range(4999)]
+    off2, adj2 = util.csr_of_undirected(n0 + 5000, np.concatenate([pairs, np.asarray(tail)]))
+    g2 = _g(off2, adj2)
+    p2 = graphs.partition_1d(g2, 1)
+    dg = graphs.device_graph(g2)
+    for root in (1, n0 + 4999):
+        ref = ob.bfs_top_down(off2, adj2, root)
+        for sparse in (True, False):
+            dg.set_sparse_levels(sparse)
+            d, st = engine.run(g2, p2, root, engine.EngineConfig(parents=True))
+            assert np.array_equal(d.d, ref), (root, sparse)
+            assert st.per_level_frontier_size == ob.level_sizes(ref)
+            assert st.traversed_edges == int(np.diff(off2)[ref != U].sum())
+            assert not ov.check_parents(off2, adj2, root, d.d, d.parents)
+    dg.set_sparse_levels(True)
