@@ -133,11 +133,14 @@ int bfb_set_checks(bfb_ctx* ctx, int flags);
  * enabled = 1 (default) uses it whenever the engine setup built its tables;
  * 0 forces the level-synchronous engine.  Applies from the next bfb_bfs. */
 int bfb_set_small_engine(bfb_ctx* ctx, int enabled);
-/* Sparse levels (one node, top-down phase 1, also inside direction-optimizing
- * runs): a level whose frontier has few edges (at most max(|V|/64, 2^16),
- * capped at 2^23) queues its phase-1 claims and
- * is committed from that queue instead of by sweeps over the whole visited
- * bitmap.  enabled = 1 (default) / 0.  Results are identical either way. */
+/* Sparse levels (top-down phase 1, also inside direction-optimizing runs; one
+ * node, several nodes of one context, and rank mode): a level whose frontier
+ * has few edges (at most max(|V|/64, 2^16), capped at 2^23) queues its
+ * phase-1 claims and is exchanged and committed from that queue instead of by
+ * sweeps over the whole visited bitmap.  With one node and top-down runs,
+ * levels of at most 2^15 frontier edges run back to back in single-CTA
+ * launches of up to 4096 levels.  enabled = 1 (default) / 0 (every level by
+ * bitmap sweeps).  Results are identical either way. */
 int bfb_set_sparse_levels(bfb_ctx* ctx, int enabled);
 /* 1 if the next top-down bfb_bfs runs on the single-CTA engine. */
 int bfb_small_engine_active(bfb_ctx* ctx);
