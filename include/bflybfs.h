@@ -138,7 +138,7 @@ int bfb_set_small_engine(bfb_ctx* ctx, int enabled);
  * has few edges (at most max(|V|/64, 2^16), capped at 2^23) queues its
  * phase-1 claims and is exchanged and committed from that queue instead of by
  * sweeps over the whole visited bitmap.  With one node and top-down runs,
- * levels of at most 2^15 frontier edges run back to back in single-CTA
+ * levels of at most 2^13 frontier edges run back to back in single-CTA
  * launches of up to 4096 levels.  enabled = 1 (default) / 0 (every level by
  * bitmap sweeps).  Results are identical either way. */
 int bfb_set_sparse_levels(bfb_ctx* ctx, int enabled);

@@ -1190,7 +1190,7 @@ __global__ void k_sparse_finalize(PartCounters* ctr, RunCounters* run) {
 }
 
 // Thin levels (one node, top-down): consecutive levels whose frontier has at
-// most kTailEdges edges run inside ONE single-CTA launch -- expand (warp per
+// most kTailEdges (2^13) edges run inside ONE single-CTA launch -- expand (warp per
 // frontier vertex, lanes over its row, atomicOr winners appended to the
 // claim queue, parents by the winners), then the commit of the claimed
 // vertices (d_local directly, start bit, q_local rows with their degree
@@ -1201,7 +1201,12 @@ __global__ void k_sparse_finalize(PartCounters* ctr, RunCounters* run) {
 // kTailMax levels, on an empty frontier, or when the frontier outgrows
 // kTailEdges; the state it leaves (q_local, counters) is the one the
 // level-synchronous passes continue from.
-constexpr int64_t kTailEdges = 1 << 15;
+// one SM expands a thin level; past ~8K edges the grid-wide passes win
+// (s29 TD, 16 roots: 2^15 309.6, 2^13 314.4, 2^12 313.3, 2^10 314.5 GTEP/s)
+#ifndef BFB_TAIL_EDGES
+#define BFB_TAIL_EDGES (1 << 13)
+#endif
+constexpr int64_t kTailEdges = BFB_TAIL_EDGES;
 constexpr int kTailMax = 4096;
 constexpr int kTailThreads = 1024;
 struct TailOut {

@@ -406,7 +406,7 @@ def test_sparse_levels_deep_path():
 
 
 def test_thin_levels_in_one_launch():
-    """Thin levels (frontier edges <= 2^15; one node, top-down) run back to
+    """Thin levels (frontier edges <= 2^13; one node, top-down) run back to
     back inside single-CTA launches of up to 4096 levels, continuing from and
     handing back to the level-synchronous passes: a 200,000-vertex path from
     one end (49 launches), and a Kronecker s16 graph with a 5,000-vertex tail
