@@ -1209,6 +1209,7 @@ __global__ void k_sparse_finalize(PartCounters* ctr, RunCounters* run) {
 constexpr int64_t kTailEdges = BFB_TAIL_EDGES;
 constexpr int kTailMax = 4096;
 constexpr int kTailThreads = 1024;
+constexpr int kTailBig = (int)(kTailEdges / 33) + 1;  // rows of > 32 edges a thin level can hold
 struct TailOut {
   int64_t levels;  // levels committed (the last may be empty: the BFS ended)
 };
@@ -1221,6 +1222,8 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(PartView v, const int6
   __shared__ unsigned long long cnt_s;
   __shared__ int64_t wsum[33];
   __shared__ int64_t carry_e, carry_r;
+  __shared__ unsigned nbig_s;
+  __shared__ uint32_t big_s[kTailBig];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = kTailThreads / 32;
   uint32_t L = level0;
@@ -1231,9 +1234,32 @@ __global__ void __launch_bounds__(kTailThreads, 1) k_tail(PartView v, const int6
     if (qn == 0 || qe > kTailEdges) break;
     if (tid == 0) cnt_s = 0;
     __syncthreads();
-    // phase 1 over q_local (rows in q_v)
-    for (int64_t k = warp; k < qn; k += nwarps) {
+    // phase 1 over q_local (rows in q_v): a thread per frontier vertex of
+    // degree <= 32 (a thin level's frontier can still hold thousands of
+    // low-degree vertices), the longer rows queued for a warp each
+    if (tid == 0) nbig_s = 0;
+    __syncthreads();
+    for (int64_t k = tid; k < qn; k += kTailThreads) {
       const uint32_t x = v.q_v[k];
+      const int64_t e0 = off[x], e1 = off[x + 1];
+      if (e1 - e0 > 32) {
+        const unsigned slot = atomicAdd(&nbig_s, 1u);
+        if (slot < kTailBig) big_s[slot] = x;
+        continue;
+      }
+      for (int64_t j = e0; j < e1; ++j) {
+        const uint32_t z = adj[j];
+        const uint32_t bit = 1u << (z & 31);
+        if (__ldcg(v.visited + (z >> 5)) & bit) continue;
+        if (atomicOr(v.visited + (z >> 5), bit) & bit) continue;
+        v.sparse_q[atomicAdd(&cnt_s, 1ull)] = z;
+        if (kParents) v.parent[z] = caller_id(v, x);
+      }
+    }
+    __syncthreads();
+    // rows longer than 32: a warp each (kTailEdges bounds them to kTailBig)
+    for (unsigned k = warp; k < min(nbig_s, (unsigned)kTailBig); k += nwarps) {
+      const uint32_t x = big_s[k];
       const int64_t e1 = off[x + 1];
       for (int64_t j = off[x] + lane; j < e1; j += 32) {
         const uint32_t z = adj[j];
