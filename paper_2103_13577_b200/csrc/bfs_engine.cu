@@ -1497,8 +1497,34 @@ __global__ void BFB_BU_LB k_bottom_up(PartView v, const uint32_t* __restrict__ a
     const int64_t wk = w0 + lane;
     const uint32_t vis_k = wk < v.whi ? v.visited[wk] : 0xFFFFFFFFu;
     const uint32_t cand_k = wk < v.whi ? owned_mask(wk, v.lo, v.hi) & ~vis_k & v.nonisol[wk] : 0u;
-    for (unsigned todo = __ballot_sync(0xffffffffu, cand_k != 0); todo; todo &= todo - 1) {
+    // the next candidate word's nbr0 / degree entries are loaded while the
+    // current word is decided (one round trip less per word)
+    unsigned todo = __ballot_sync(0xffffffffu, cand_k != 0);
+    uint32_t fx_n = 0;
+    uint16_t dg_n = 0;
+    if (todo) {
+      const int jn = __ffs(todo) - 1;
+      const uint32_t cn = __shfl_sync(0xffffffffu, cand_k, jn);
+      const int64_t un = ((w0 + jn) << 5) + lane;
+      if ((cn >> lane) & 1u) {
+        fx_n = __ldg(v.nbr0 + un);
+        dg_n = __ldg(v.deg16 + un);
+      }
+    }
+    for (; todo; ) {
       const int jw = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t fx = fx_n;
+      const uint16_t dg = dg_n;
+      if (todo) {
+        const int jn = __ffs(todo) - 1;
+        const uint32_t cn = __shfl_sync(0xffffffffu, cand_k, jn);
+        const int64_t un = ((w0 + jn) << 5) + lane;
+        if ((cn >> lane) & 1u) {
+          fx_n = __ldg(v.nbr0 + un);
+          dg_n = __ldg(v.deg16 + un);
+        }
+      }
       const int64_t w = w0 + jw;
       const uint32_t vis = __shfl_sync(0xffffffffu, vis_k, jw);
       const uint32_t cand = __shfl_sync(0xffffffffu, cand_k, jw);
@@ -1512,8 +1538,7 @@ __global__ void BFB_BU_LB k_bottom_up(PartView v, const uint32_t* __restrict__ a
         // the two lowest-id neighbours (hubs, on Kronecker graphs) decide most
         // candidates -- all of those with degree <= 2 -- from a per-vertex
         // table read coalesced across the warp; only the rest load the row
-        const uint32_t fx = __ldg(v.nbr0 + u);
-        more = __ldg(v.deg16 + u) > 2;
+        more = dg > 2;
         ++ex;
         if ((front[fx >> 5] >> (fx & 31)) & 1u) {
           found = true;
