@@ -315,7 +315,7 @@ def main_single(args):
         "bottom_up_edges_examined_per_traversed":
             round(sum(st.edges_examined for st in do) / max(1, do_edges), 4),
         "note": "same graph, roots, parents and levels (bit-identical); phase 1 switches "
-                "top-down/bottom-up by Beamer's rule (alpha 5, beta 1024, tuned on this graph; "
+                "top-down/bottom-up by Beamer's rule (alpha 14, beta 64, tuned on this graph and s24 ef16; "
                 "Beamer's CPU values are 14, 24); TEPS counts the same E_trav"}
 
     # e2e: the public API call (engine.run) with host-resident results, every

@@ -147,8 +147,8 @@ int bfb_small_engine_active(bfb_ctx* ctx);
 /* Phase-1 direction (paper contribution 3; SPEC.md:172 keeps
  * the slot): 0 = top-down (Alg. 2, default), 1 = direction-optimizing with
  * Beamer's switch (TD->BU when frontier edges > unexplored edges / alpha,
- * BU->TD when frontier < |V| / beta; defaults alpha 5, beta 1024, tuned on
- * Kronecker s29 -- Beamer's CPU values are 14 and 24), 2 = bottom-up at every
+ * BU->TD when frontier < |V| / beta; defaults alpha 14, beta 64, tuned on
+ * Kronecker s29 ef8 and s24 ef16 -- Beamer's CPU values are 14 and 24), 2 = bottom-up at every
  * level (testing).
  * Levels, frontier sizes and traversed edges are identical in all modes (the
  * exchange volumes differ: bottom-up discoveries are owned vertices only).

@@ -262,7 +262,7 @@ struct bfb_ctx {
   bool timing = false;
   int checks = 0;                     // bfb_set_checks: 1 = frontier agreement after phase 2
   int direction = 0;                  // 0 top-down, 1 direction-optimizing, 2 bottom-up
-  double do_alpha = 5.0, do_beta = 1024.0;  // tuned at s29 (Beamer: 14, 24)
+  double do_alpha = 14.0, do_beta = 64.0;  // tuned at s29 / s24 (Beamer: 14, 24)
   bool have_run = false;
   int64_t last_root = -1;
   int64_t last_levels = 0;

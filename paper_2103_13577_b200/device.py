@@ -229,7 +229,7 @@ class DeviceGraph:
     def num_parts(self):
         return len(self._engine_key[0]) - 1 if self._engine_key else 0
 
-    def set_direction(self, direction="top-down", alpha=5.0, beta=1024.0):
+    def set_direction(self, direction="top-down", alpha=14.0, beta=64.0):
         """Phase-1 direction: "top-down" (Alg. 2), "optimizing" (Beamer
         switch) or "bottom-up"; levels are identical in every mode."""
         if direction not in _lib.DIRECTION:

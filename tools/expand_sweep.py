@@ -16,7 +16,7 @@ roots = graphs.sample_roots(g, int(os.environ.get("SW_ROOTS", "6")))
 for parents, direction in ((False, "top-down"), (True, "top-down"), (True, "optimizing"), (False, "optimizing")):
     P = int(os.environ.get("SW_PARTS", "1"))
     dg.setup(dg.partition_1d(P), min(2, P), "butterfly", parents=parents)
-    dg.set_direction(direction, float(os.environ.get("SW_ALPHA", "5")), float(os.environ.get("SW_BETA", "1024")))
+    dg.set_direction(direction, float(os.environ.get("SW_ALPHA", "14")), float(os.environ.get("SW_BETA", "64")))
     dg.set_timing(True)
     dg.bfs(int(roots[0]), levels=False)
     t = []; ex = []; cm = []; xc = []; mp = []
