@@ -235,7 +235,8 @@ def config_of(args, n_gpus, fanout, parents):
         "scale": args.scale, "edge_factor": args.edge_factor, "seed": 1, "roots": args.roots,
         "roots_timed": args.roots, "num_parts": n_gpus, "fanout": fanout, "strategy": "butterfly",
         "parents": parents, "parallelism": f"1D vertex partition x{n_gpus}",
-        "l2": "inputs larger than L2 (CSR of s29 ~38 GB vs 126 MB L2)",
+        "l2": f"inputs larger than L2 (CSR of s{args.scale} ef{args.edge_factor} "
+              f"~{(8 * args.edge_factor + 8) * 2 ** args.scale / 1e9:.1f} GB vs 126 MB L2)",
         "graph_build": "on device (bit-exact generator, CSR, partition)",
     }
 
