@@ -1124,7 +1124,7 @@ __global__ void BFB_WRITE_LB k_commit_write(PartView v, const int64_t* __restric
 // the packed totals into the next frontier's counters.
 constexpr int kPackShift = 40;
 #ifndef BFB_SPARSE_SHIFT
-#define BFB_SPARSE_SHIFT 6  // sparse levels: at most n >> this many frontier edges
+#define BFB_SPARSE_SHIFT 5  // sparse levels: at most n >> this many frontier edges
 #endif
 #ifndef BFB_SPARSE_CAP
 #define BFB_SPARSE_CAP (1 << 23)  // ... and at most this many (the packed row count is 24 bits)
