@@ -39,9 +39,20 @@ constexpr int kExpandBlock = 256;
 // n >> BFB_PASS_SHIFT (s29 sweeps: first pass build 4 224.4, 6 226.4, 8
 // 226.9, 10 226.4, always 221.1 GTEP/s; with the batched, counter-scheduled
 // pass and expand 8 243.6, 10 245.4, 12 245.0, 16 244.0).
+// With a floor of BFB_PASS_MIN vertices: s24 ef16 ran its second level with
+// the pass at 4096-16383 reached vertices and lost 6% to its row scans
+// (TD 223.5 -> 236.4 GTEP/s with the floor; s29 unchanged).
 #ifndef BFB_PASS_SHIFT
 #define BFB_PASS_SHIFT 12
 #endif
+#ifndef BFB_PASS_MIN
+#define BFB_PASS_MIN (1 << 14)
+#endif
+// (the floor is at most n / 64, so small graphs still run the pass)
+constexpr int64_t pass_min_reached(int64_t n) {
+  const int64_t floor = (int64_t)BFB_PASS_MIN < (n >> 6) ? (int64_t)BFB_PASS_MIN : (n >> 6);
+  return (n >> BFB_PASS_SHIFT) > floor ? (n >> BFB_PASS_SHIFT) : floor;
+}
 #ifndef BFB_EXPAND_ITEMS
 #define BFB_EXPAND_ITEMS 12
 #endif
@@ -2505,7 +2516,7 @@ int engine_bfs(bfb_ctx* ctx, int64_t root, uint32_t* levels_out, int64_t* parent
     // row scans.
     const bool parent_pass = ctx->want_parents && !bottom_up &&
                              prev_frontier >= std::max<int64_t>(1, n >> 12) &&
-                             reached >= (n >> BFB_PASS_SHIFT);
+                             reached >= pass_min_reached(n);
     const bool expand_parents = ctx->want_parents && (!parent_pass || sparse);
     // Phase 1
     const bool part_timing = ctx->timing && P > 1;
@@ -3436,7 +3447,7 @@ int rank_bfs(bfb_ctx* ctx, int64_t root, int64_t* sizes_out, int64_t max_levels,
     // nodes' store-free phase 1 found)
     const bool parent_pass = ctx->want_parents && !bottom_up &&
                              prev_frontier >= std::max<int64_t>(1, n >> 12) &&
-                             D->reached >= (n >> BFB_PASS_SHIFT);
+                             D->reached >= pass_min_reached(n);
     if (bottom_up) {
       const unsigned bg = grid_cap(std::max<int64_t>(1, v.whi - v.wlo), 256, sms, 8);
       unsigned long long* ex = (unsigned long long*)&ctx->run.p->edges_examined;
