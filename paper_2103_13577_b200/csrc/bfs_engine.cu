@@ -39,14 +39,16 @@ constexpr int kExpandBlock = 256;
 // n >> BFB_PASS_SHIFT (s29 sweeps: first pass build 4 224.4, 6 226.4, 8
 // 226.9, 10 226.4, always 221.1 GTEP/s; with the batched, counter-scheduled
 // pass and expand 8 243.6, 10 245.4, 12 245.0, 16 244.0).
-// With a floor of BFB_PASS_MIN vertices: s24 ef16 ran its second level with
-// the pass at 4096-16383 reached vertices and lost 6% to its row scans
-// (TD 223.5 -> 236.4 GTEP/s with the floor; s29 unchanged).
+// With a floor of BFB_PASS_MIN vertices: on s22-s26 graphs the level after a
+// small frontier ran the pass with few hubs in `start`, and its row scans
+// cost more than phase-1 stores (16 roots, TD GTEP/s, floor none / 2^14 /
+// 2^16 / 2^18: s22 ef16 93 / 101 / 106 / 107, s24 ef16 224 / 236 / 242 / 246,
+// s26 269 / - / 276 / 277, s29 315 / 315 / 315 / 313).
 #ifndef BFB_PASS_SHIFT
 #define BFB_PASS_SHIFT 12
 #endif
 #ifndef BFB_PASS_MIN
-#define BFB_PASS_MIN (1 << 14)
+#define BFB_PASS_MIN (1 << 16)
 #endif
 // (the floor is at most n / 64, so small graphs still run the pass)
 constexpr int64_t pass_min_reached(int64_t n) {
