@@ -1703,37 +1703,37 @@ __device__ __forceinline__ void store_unit_levels(const LevelSlices& L, int64_t 
 // kLevelBits written directly), kLv8None unreached.  A quarter of the bytes of
 // the uint32 form, written and then gathered.
 constexpr uint32_t kLv8None = 0xFFu, kLv8Keep = 0xFEu;
-__device__ __forceinline__ void store_unit_levels8(const LevelSlices& L, int64_t w0,
+// Each lane turns its own word's slices into 32 bytes (two 16-byte stores),
+// no shuffles: 469 -> 286 us at s29 (ncu), DO +2.5%, against the layout that
+// shuffled each word's slices to 8 lanes for 128-byte contiguous warp stores
+// (the kernel was issue-bound on the shuffles at 39% occupancy).
+__device__ __forceinline__ void store_word_levels8(const LevelSlices& L, int64_t wk, int64_t nwords,
                                                    uint8_t* __restrict__ lv8, int64_t n) {
-  const int lane = threadIdx.x & 31;
-  const int sub = lane >> 3, b0 = (lane & 7) * 4;
-#pragma unroll 2
-  for (int q = 0; q < 8; ++q) {
-    const int j = q * 4 + sub;
-    uint32_t sl[5];
+  if (wk >= nwords) return;
+  const int64_t u0 = wk << 5;
+  uint32_t out[8];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) sl[k] = __shfl_sync(0xffffffffu, L.s[k], j) >> b0;
-    const uint32_t aj = __shfl_sync(0xffffffffu, L.any, j) >> b0;
-    const uint32_t vj = __shfl_sync(0xffffffffu, L.vis, j) >> b0;
-    const int64_t u0 = ((w0 + j) << 5) + b0;
-    if (u0 >= n) continue;
+  for (int q = 0; q < 8; ++q) {
     uint32_t bytes = 0;
 #pragma unroll
-    for (int k = 0; k < 5; ++k) bytes |= spread4(sl[k] & 0xFu) << k;
-    const uint32_t f = aj & 0xFu;
-    const uint32_t keep = spread4(vj & ~f & 0xFu) * 0xFFu;  // visited, in no bitmap
-    bytes |= ~(spread4(f) * 0xFFu);                         // 0xFF where in no bitmap
-    bytes &= ~keep | (kLv8Keep * 0x01010101u);              // ... 0xFE where kept
-    if (u0 + 4 <= n) {
-      *reinterpret_cast<uint32_t*>(lv8 + u0) = bytes;
-    } else {
-      for (int t = 0; u0 + t < n; ++t) lv8[u0 + t] = (uint8_t)(bytes >> (8 * t));
-    }
+    for (int k = 0; k < 5; ++k) bytes |= spread4((L.s[k] >> (4 * q)) & 0xFu) << k;
+    const uint32_t f = (L.any >> (4 * q)) & 0xFu;
+    const uint32_t keep = spread4((L.vis >> (4 * q)) & ~f & 0xFu) * 0xFFu;
+    bytes |= ~(spread4(f) * 0xFFu);
+    bytes &= ~keep | (kLv8Keep * 0x01010101u);
+    out[q] = bytes;
+  }
+  if (u0 + 32 <= n) {
+    uint4* d = reinterpret_cast<uint4*>(lv8 + u0);
+    d[0] = make_uint4(out[0], out[1], out[2], out[3]);
+    d[1] = make_uint4(out[4], out[5], out[6], out[7]);
+  } else {
+    for (int t = 0; u0 + t < n; ++t) lv8[u0 + t] = (uint8_t)(out[t >> 2] >> (8 * (t & 3)));
   }
 }
 
 // Units are taken two at a time so each warp has both units' bitmap loads in
-// flight before the stores.  lv8 != nullptr: the byte form instead of d_local.
+// flight before the stores (uint32 d_local; the byte form is k_levels8_from_bits).
 #ifdef BFB_LEVELS_MINB
 #define BFB_LEVELS_LB __launch_bounds__(256, BFB_LEVELS_MINB)
 #else
@@ -1742,8 +1742,7 @@ __device__ __forceinline__ void store_unit_levels8(const LevelSlices& L, int64_t
 __global__ void BFB_LEVELS_LB k_levels_from_bits(const uint32_t* __restrict__ lvbits,
                                                           int64_t pad, int nl, uint32_t valid,
                                                           const uint32_t* __restrict__ visited,
-                                                          uint32_t* __restrict__ level,
-                                                          uint8_t* __restrict__ lv8, int64_t n) {
+                                                          uint32_t* __restrict__ level, int64_t n) {
   const int lane = threadIdx.x & 31;
   const int64_t nwords = (n + 31) / 32;
   const int64_t nunits = (nwords + 31) / 32;
@@ -1756,13 +1755,23 @@ __global__ void BFB_LEVELS_LB k_levels_from_bits(const uint32_t* __restrict__ lv
                       A);
     load_level_slices(lvbits, pad, nl, valid, visited, unit2 * 32 + lane,
                       unit2 < nunits && unit2 * 32 + lane < nwords, B);
-    if (lv8) {
-      store_unit_levels8(A, unit * 32, lv8, n);
-      if (unit2 < nunits) store_unit_levels8(B, unit2 * 32, lv8, n);
-    } else {
-      store_unit_levels(A, unit * 32, level, n);
-      if (unit2 < nunits) store_unit_levels(B, unit2 * 32, level, n);
-    }
+    store_unit_levels(A, unit * 32, level, n);
+    if (unit2 < nunits) store_unit_levels(B, unit2 * 32, level, n);
+  }
+}
+
+// Byte form: one word per thread, 8 blocks per SM (32 registers): 284 ->
+// 261 us at s29 against two units per warp at 40 registers.
+__global__ void __launch_bounds__(256, 8) k_levels8_from_bits(const uint32_t* __restrict__ lvbits,
+                                                            int64_t pad, int nl, uint32_t valid,
+                                                            const uint32_t* __restrict__ visited,
+                                                            uint8_t* __restrict__ lv8, int64_t n) {
+  const int64_t nwords = (n + 31) / 32;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    LevelSlices A;
+    load_level_slices(lvbits, pad, nl, valid, visited, w, true, A);
+    store_word_levels8(A, w, nwords, lv8, n);
   }
 }
 
@@ -1961,10 +1970,17 @@ int launch_materialise_levels(bfb_ctx* ctx, Part& p, int64_t last_level, cudaStr
                               uint8_t* lv8 = nullptr) {
   const int64_t pad = (int64_t)(p.lvbits.n / kLevelBits);
   const int nl = (int)std::min<int64_t>(last_level, kLevelBits - 1);
+  if (lv8) {
+    k_levels8_from_bits<<<resident_grid(k_levels8_from_bits, (ctx->g.n + 31) / 32, 256,
+                                        ctx->num_sms),
+                          256, 0, s>>>(p.lvbits.p, pad, nl, ctx->lvbits_valid, p.visited.p, lv8,
+                                       ctx->g.n);
+    return 1;
+  }
   k_levels_from_bits<<<resident_grid(k_levels_from_bits, (ctx->g.n + 31) / 32, 256,
                                      ctx->num_sms),
                        256, 0, s>>>(p.lvbits.p, pad, nl, ctx->lvbits_valid, p.visited.p, p.level.p,
-                                    lv8, ctx->g.n);
+                                    ctx->g.n);
   return 1;
 }
 

@@ -11,4 +11,6 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 bash tools/profile_r02.sh > gpurun_out/profile.log 2>&1
 ncu --set full --import-source on --clock-control none -f -k regex:k_output -c 1 -o gpurun_out/kout python tools/profile_bfs.py --runs 0 --parents 1 > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/kout.ncu-rep > gpurun_out/kout.txt 2>&1
+ncu --set full --import-source on --clock-control none -f -k regex:k_levels8 -c 1 -o gpurun_out/lfb python tools/profile_bfs.py --runs 0 --parents 1 > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/lfb.ncu-rep > gpurun_out/lfb.txt 2>&1
 tail -3 gpurun_out/tests.log; tail -c 600 gpurun_out/bench.json; tail -c 300 gpurun_out/bench_ref.json
