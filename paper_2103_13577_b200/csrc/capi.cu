@@ -2,11 +2,6 @@
 // reporting, the host-side butterfly schedule, and dispatch to the device code.
 #include <cstdio>
 #include <cstring>
-#include <cstdlib>
-#include <mutex>
-#include <unordered_map>
-
-#include <sys/mman.h>
 
 #include "bfb_internal.cuh"
 
@@ -123,35 +118,9 @@ int bfb_device_count(int* count_out) {
   return BFB_OK;
 }
 
-namespace {
-// Read-out destinations on 2 MB pages (BFB_HOST_HUGE=1): anonymous mapping,
-// MADV_HUGEPAGE, then page-locked with cudaHostRegister.
-std::mutex g_huge_mu;
-std::unordered_map<void*, size_t> g_huge;
-void* huge_alloc(size_t bytes) {
-  const size_t len = (bytes + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
-  void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-  if (p == MAP_FAILED) return nullptr;
-  madvise(p, len, MADV_HUGEPAGE);
-  if (cudaHostRegister(p, len, cudaHostRegisterPortable) != cudaSuccess) {
-    cudaGetLastError();
-    munmap(p, len);
-    return nullptr;
-  }
-  std::lock_guard<std::mutex> lk(g_huge_mu);
-  g_huge[p] = len;
-  return p;
-}
-}  // namespace
-
 int bfb_host_alloc(size_t bytes, void** ptr_out) {
   if (!ptr_out) return fail(BFB_ERR_INVALID, "null output");
   *ptr_out = nullptr;
-  const char* hv = std::getenv("BFB_HOST_HUGE");
-  if (hv && hv[0] == '1' && bytes >= (8u << 20)) {
-    *ptr_out = huge_alloc(bytes);
-    if (*ptr_out) return BFB_OK;
-  }
   cudaError_t e = cudaHostAlloc(ptr_out, bytes ? bytes : 1, cudaHostAllocPortable);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -161,18 +130,7 @@ int bfb_host_alloc(size_t bytes, void** ptr_out) {
 }
 
 void bfb_host_free(void* ptr) {
-  if (!ptr) return;
-  {
-    std::lock_guard<std::mutex> lk(g_huge_mu);
-    auto it = g_huge.find(ptr);
-    if (it != g_huge.end()) {
-      cudaHostUnregister(ptr);
-      munmap(ptr, it->second);
-      g_huge.erase(it);
-      return;
-    }
-  }
-  cudaFreeHost(ptr);
+  if (ptr) cudaFreeHost(ptr);
 }
 
 int bfb_num_rounds(int num_nodes, int fanout, int* rounds_out) {
