@@ -1779,58 +1779,73 @@ __global__ void __launch_bounds__(256, 8) k_levels8_from_bits(const uint32_t* __
 // Results in the caller's ids (relabelled engine graph): out[v] = engine
 // result at perm[v], from the byte form of d_local (lv8; kLv8Keep -> the
 // uint32 d_local).  The relabel keeps each degree class in the caller's
-// order, so consecutive v gather from a few ascending streams (isolated
-// vertices: one stream of UNREACHED); each thread keeps kOutBatch vertices'
-// loads in flight (the perm -> gather chain is latency-bound otherwise: 6.6 ms
-// vs 1.x ms at s29).  Skipping the gathers of isolated vertices (a part
-// lookup per vertex) and capping registers for occupancy measured slower
-// (1.88 -> 2.23 ms at s29): their gathers are cheap sequential streams.
+// order, so the lanes of a warp (consecutive v) gather from one ascending
+// stream most of the time (isolated vertices: one stream of UNREACHED).
 // Parents are stored in the caller's ids already; an unreached vertex gets
 // none (this also masks a single node's stale entries).  out_level ==
 // nullptr: parents only.
-// vertices per thread in flight x resident blocks per SM (s29, 16 roots,
-// TD / DO GTEP/s): 8 x 4 (62 regs) 298.7 / 995, 16 x 2 269.7 / 731,
-// 12 x 3 292.6 / 927, 2 x 8 300 / 1021, 4 x 6 300 / 1014, 4 x 8 (32 regs,
-// full occupancy) 305 / 1075: the gathers are latency-bound, warps beat
-// per-thread batches
-#ifndef BFB_OUT_BATCH
-#define BFB_OUT_BATCH 4
-#endif
-#ifndef BFB_OUT_MINB
-#define BFB_OUT_MINB 8
-#endif
-constexpr int kOutBatch = BFB_OUT_BATCH;
-__global__ void __launch_bounds__(256, BFB_OUT_MINB) k_output(const uint32_t* __restrict__ perm,
-                                                const uint8_t* __restrict__ lv8,
-                                                const uint32_t* __restrict__ level,
-                                                const uint32_t* __restrict__ parent,
-                                                uint32_t* __restrict__ out_level,
-                                                uint32_t* __restrict__ out_parent, int64_t n) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < n;
-       v0 += stride * kOutBatch) {
-    uint32_t p[kOutBatch], l[kOutBatch], q[kOutBatch];
+// Each block takes 1024 vertices per step (4 per thread, lane-consecutive);
+// the next step's perm entries are copied into shared memory by cp.async
+// while this step gathers, so perm is off the per-vertex dependence chain
+// (perm -> byte level -> parent -> store).  s29, ncu: 1.80 -> 1.55 ms, DO
+// 1180 -> 1226 GTEP/s, against the register-only kernel whose best setting
+// was 4 vertices per thread at 8 blocks/SM (prefetching perm in registers
+// spilled at 32 registers; 4 consecutive vertices per thread with 16-byte
+// stores: 1.66 ms, the warp's gathers spread over 4x the lines).
+constexpr int kOutChunk = 1024;  // vertices per block per step (256 threads x 4)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n"); }
+__global__ void __launch_bounds__(256, 8) k_output(const uint32_t* __restrict__ perm,
+                                                   const uint8_t* __restrict__ lv8,
+                                                   const uint32_t* __restrict__ level,
+                                                   const uint32_t* __restrict__ parent,
+                                                   uint32_t* __restrict__ out_level,
+                                                   uint32_t* __restrict__ out_parent, int64_t n) {
+  __shared__ __align__(16) uint32_t sp[2][kOutChunk];
+  const int64_t nfull = n / kOutChunk;  // whole chunks; the remainder below
+  const int t4 = threadIdx.x * 4;
+  int64_t c = blockIdx.x;  // uniform per block: the barriers below are safe
+  if (c < nfull) cp_async16(&sp[0][t4], perm + c * kOutChunk + t4);
+  cp_async_commit();
+  for (int b = 0; c < nfull; c += gridDim.x, b ^= 1) {
+    const int64_t cn = c + gridDim.x;
+    if (cn < nfull) cp_async16(&sp[b ^ 1][t4], perm + cn * kOutChunk + t4);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();  // every thread's copy of this step's entries landed
+    uint32_t p[4], l[4], q[4];
 #pragma unroll
-    for (int k = 0; k < kOutBatch; ++k) {
-      const int64_t v = v0 + k * stride;
-      p[k] = v < n ? __ldg(perm + v) : 0u;
-    }
+    for (int k = 0; k < 4; ++k) p[k] = sp[b][k * 256 + threadIdx.x];
 #pragma unroll
-    for (int k = 0; k < kOutBatch; ++k) l[k] = v0 + k * stride < n ? __ldg(lv8 + p[k]) : kLv8None;
+    for (int k = 0; k < 4; ++k) l[k] = __ldg(lv8 + p[k]);
 #pragma unroll
-    for (int k = 0; k < kOutBatch; ++k)
+    for (int k = 0; k < 4; ++k)
       l[k] = l[k] == kLv8None ? kNone : (l[k] == kLv8Keep ? __ldg(level + p[k]) : l[k]);
+    const int64_t v = c * kOutChunk + threadIdx.x;
     if (out_parent) {
 #pragma unroll
-      for (int k = 0; k < kOutBatch; ++k) q[k] = l[k] != kNone ? __ldg(parent + p[k]) : kNone;
-    }
+      for (int k = 0; k < 4; ++k) q[k] = l[k] != kNone ? __ldg(parent + p[k]) : kNone;
 #pragma unroll
-    for (int k = 0; k < kOutBatch; ++k) {
-      const int64_t v = v0 + k * stride;
-      if (v < n) {
-        if (out_level) out_level[v] = l[k];
-        if (out_parent) out_parent[v] = q[k];
-      }
+      for (int k = 0; k < 4; ++k) out_parent[v + k * 256] = q[k];
+    }
+    if (out_level) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) out_level[v + k * 256] = l[k];
+    }
+    __syncthreads();  // buffer b is refilled by the next step's copies
+  }
+  // remainder (< kOutChunk vertices): block 0, one vertex per thread
+  if (blockIdx.x == 0) {
+    for (int64_t v = nfull * kOutChunk + threadIdx.x; v < n; v += blockDim.x) {
+      const uint32_t pp = perm[v];
+      uint32_t lv = lv8[pp];
+      lv = lv == kLv8None ? kNone : (lv == kLv8Keep ? level[pp] : lv);
+      if (out_level) out_level[v] = lv;
+      if (out_parent) out_parent[v] = lv != kNone ? parent[pp] : kNone;
     }
   }
 }
@@ -1991,7 +2006,7 @@ int launch_output(bfb_ctx* ctx, Part& p, int64_t last_level, const uint32_t* par
   // (the byte form of d_local: levels=false reuses the run's, for the mask)
   if (levels) k += launch_materialise_levels(ctx, p, last_level, s, ctx->lv8.p);
   const int64_t n = ctx->g.n;
-  k_output<<<grid_cap((n + kOutBatch - 1) / kOutBatch, 256, ctx->num_sms, 8), 256, 0, s>>>(
+  k_output<<<grid_cap((n + kOutChunk - 1) / kOutChunk * 256, 256, ctx->num_sms, 8), 256, 0, s>>>(
       ctx->perm.p, ctx->lv8.p, p.level.p, parent, levels ? ctx->out_level.p : nullptr,
       parent ? ctx->out_parent.p : nullptr, n);
   return k + 1;
