@@ -1785,38 +1785,52 @@ __global__ void __launch_bounds__(256, 8) k_levels8_from_bits(const uint32_t* __
 // none (this also masks a single node's stale entries).  out_level ==
 // nullptr: parents only.
 // Each block takes 1024 vertices per step (4 per thread, lane-consecutive);
-// the next step's perm entries are copied into shared memory by cp.async
-// while this step gathers, so perm is off the per-vertex dependence chain
-// (perm -> byte level -> parent -> store).  s29, ncu: 1.80 -> 1.55 ms, DO
-// 1180 -> 1226 GTEP/s, against the register-only kernel whose best setting
+// the next step's perm entries are copied into shared memory by one TMA bulk
+// copy while this step gathers, so perm is off the per-vertex dependence
+// chain (perm -> byte level -> parent -> store).  s29, ncu: 1.80 -> 1.55 ms,
+// DO 1180 -> 1226 GTEP/s (per-thread 16-byte cp.async copies measured the
+// same as the bulk copy), against the register-only kernel whose best setting
 // was 4 vertices per thread at 8 blocks/SM (prefetching perm in registers
 // spilled at 32 registers; 4 consecutive vertices per thread with 16-byte
 // stores: 1.66 ms, the warp's gathers spread over 4x the lines).
 constexpr int kOutChunk = 1024;  // vertices per block per step (256 threads x 4)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n"); }
 __global__ void __launch_bounds__(256, 8) k_output(const uint32_t* __restrict__ perm,
                                                    const uint8_t* __restrict__ lv8,
                                                    const uint32_t* __restrict__ level,
                                                    const uint32_t* __restrict__ parent,
                                                    uint32_t* __restrict__ out_level,
                                                    uint32_t* __restrict__ out_parent, int64_t n) {
-  __shared__ __align__(16) uint32_t sp[2][kOutChunk];
+  __shared__ __align__(128) uint32_t sp[2][kOutChunk];
   const int64_t nfull = n / kOutChunk;  // whole chunks; the remainder below
-  const int t4 = threadIdx.x * 4;
   int64_t c = blockIdx.x;  // uniform per block: the barriers below are safe
-  if (c < nfull) cp_async16(&sp[0][t4], perm + c * kOutChunk + t4);
-  cp_async_commit();
-  for (int b = 0; c < nfull; c += gridDim.x, b ^= 1) {
+  // one bulk copy (TMA engine) of 4 KB per step, issued by thread 0, landing
+  // on an mbarrier per buffer (phase parity flips with each use)
+  __shared__ __align__(8) unsigned long long bar[2];
+  const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&bar[0]);
+  auto bulk = [&](int buf, int64_t chunk) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(&sp[buf][0]);
+    const unsigned mb = bar0 + 8u * (unsigned)buf;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                 "r"(kOutChunk * 4) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(perm + chunk * kOutChunk), "r"(kOutChunk * 4), "r"(mb) : "memory");
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8u));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && c < nfull) bulk(0, c);
+  for (int b = 0, use = 0; c < nfull; c += gridDim.x, b ^= 1, ++use) {
     const int64_t cn = c + gridDim.x;
-    if (cn < nfull) cp_async16(&sp[b ^ 1][t4], perm + cn * kOutChunk + t4);
-    cp_async_commit();
-    cp_async_wait1();
-    __syncthreads();  // every thread's copy of this step's entries landed
+    if (threadIdx.x == 0 && cn < nfull) bulk(b ^ 1, cn);
+    const unsigned parity = (unsigned)(use >> 1) & 1u;
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT%=;\n}\n" ::"r"(bar0 + 8u * (unsigned)b),
+        "r"(parity) : "memory");
     uint32_t p[4], l[4], q[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) p[k] = sp[b][k * 256 + threadIdx.x];
