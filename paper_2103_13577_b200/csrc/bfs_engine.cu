@@ -1712,16 +1712,36 @@ __device__ __forceinline__ void store_word_levels8(const LevelSlices& L, int64_t
   if (wk >= nwords) return;
   const int64_t u0 = wk << 5;
   uint32_t out[8];
+  // 8x8 bit transposes (rows = level bit-planes 0..4, "in no bitmap",
+  // "kept"; one 8x8 block per byte): row r byte c then holds vertex 8c + r.
+  // 3 delta-swap stages + 3 byte permutes per output word: 261 -> 217 us at
+  // s29 against spreading each nibble of each plane with a multiply.
+  uint32_t r[8] = {L.s[0], L.s[1], L.s[2], L.s[3], L.s[4], ~L.any, L.vis & ~L.any, 0u};
+#pragma unroll
+  for (int d = 4, st = 0; st < 3; d >>= 1, ++st) {
+    const uint32_t m = d == 4 ? 0x0F0F0F0Fu : (d == 2 ? 0x33333333u : 0x55555555u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i & d) continue;
+      const uint32_t t = ((r[i] >> d) ^ r[i + d]) & m;
+      r[i + d] ^= t;
+      r[i] ^= t << d;
+    }
+  }
+  // bit 5 (in no bitmap) -> 0xFF, or 0xFE with bit 6 (kept)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t m5 = ((r[i] >> 5) & 0x01010101u) * 0xFFu;
+    const uint32_t m6 = (r[i] >> 6) & 0x01010101u;
+    r[i] = (r[i] & ~m5) | (m5 ^ m6);
+  }
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    uint32_t bytes = 0;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) bytes |= spread4((L.s[k] >> (4 * q)) & 0xFu) << k;
-    const uint32_t f = (L.any >> (4 * q)) & 0xFu;
-    const uint32_t keep = spread4((L.vis >> (4 * q)) & ~f & 0xFu) * 0xFFu;
-    bytes |= ~(spread4(f) * 0xFFu);
-    bytes &= ~keep | (kLv8Keep * 0x01010101u);
-    out[q] = bytes;
+    const int c = q >> 1, r0 = (q & 1) * 4;
+    const uint32_t sel = (uint32_t)c | ((uint32_t)(4 + c) << 4);
+    const uint32_t lo = __byte_perm(r[r0], r[r0 + 1], sel);
+    const uint32_t hi = __byte_perm(r[r0 + 2], r[r0 + 3], sel);
+    out[q] = __byte_perm(lo, hi, 0x5410);
   }
   if (u0 + 32 <= n) {
     uint4* d = reinterpret_cast<uint4*>(lv8 + u0);
